@@ -1,0 +1,217 @@
+/*
+ * owq.h -- C ABI of libowq.so, the B200 (sm_100a) hot path of OWQ
+ * (Outlier-aware Weight Quantization, arXiv 2306.02272).
+ *
+ * The operation (Sec. 4; Sec. 5.4):
+ *
+ *   y = W_hat x,   W_hat = (zero-filled b-bit matrix) + (fp16 weak columns)
+ *
+ *   "we store a complete low-precision matrix with zero-filled weak columns.
+ *    Additionally, we store the weak columns as fp16 and use an extra single
+ *    16-bit integer per column [...] the output of the matrix multiplication can
+ *    be calculated as the sum of (zero-filled quantized weight matrix x fp16
+ *    activation matrix) and (fp16 weak columns x corresponding fp16 activation
+ *    channels)."
+ *
+ *   y[b][i] = sum_{j not weak} s[i][g(j)] * (q[i][j] - z[i][g(j)]) * x[b][j]
+ *           + sum_{t < k} v[i][t] * x[b][idx[t]]
+ *
+ * W in R^{C_out x C_in}.  x is row-major [B][C_in] and y is [B][C_out]
+ * (the transpose of the paper's C_in x N layout, reading s18).
+ * g(j) = j / group_size (group_size 0 = one scale/zero per output row; P:362-388
+ * for grouped grids).  Scale s and zero z are fp16; z is an integer code
+ * (readings s7, s10).  Weak-column indices are u16, so
+ * C_in <= 65536.
+ *
+ * Conventions
+ *  - Every entry point validates on the host and returns an owq_status; no C++
+ *    exception crosses the ABI.  Device calls are asynchronous on the given
+ *    stream (cudaStream_t passed as void*; NULL = legacy default stream); a
+ *    launch failure is returned as OWQ_ERR_CUDA, a fault inside a kernel
+ *    surfaces at the caller's next synchronisation.
+ *  - All buffers are caller-owned.  "d_" = device pointer, "h_" = host pointer.
+ *    Nothing on the hot path (owq_gemv, owq_gemm_small_batch, owq_tp_gemv)
+ *    allocates device memory or synchronises with the host.
+ *  - fp16 values cross the ABI as uint16_t bit patterns (IEEE binary16) so this
+ *    header is plain C99 with no CUDA headers.
+ *
+ * Device layout (the "packed blob", produced only by owq_pack / owq_pack_host;
+ * version OWQ_LAYOUT_VERSION, self-describing: a 256-byte header repeats the
+ * shape, so every call re-checks shape agreement).  Rows are grouped in
+ * row-blocks of 64 (the last one padded); columns in super-steps of 64 (the
+ * last one padded).  Per row-block the record holds its super-steps followed
+ * by its weak-column chunks (8 columns each, mma-fragment order; the ragged
+ * last chunk row-major, unpadded), so any run of items is one contiguous TMA
+ * bulk copy.
+ * Inside a super-step, codes are ordered for the mma.sync m16n8k16 A-fragment
+ * of each lane and pre-positioned inside 32-bit words so that one LOP3 with an
+ * fp16 exponent "magic" yields two exact values 1024 + q*2^p.
+ * gives the exact bit map; owq_unpack_codes / owq_blob_decode_host invert it.
+ */
+#ifndef OWQ_H_
+#define OWQ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OWQ_LAYOUT_VERSION 1
+#define OWQ_MAX_BATCH 16
+
+typedef enum {
+  OWQ_OK = 0,
+  OWQ_ERR_INVALID_ARG = 1,     /* NULL pointer, non-positive size, bad mode      */
+  OWQ_ERR_UNSUPPORTED = 2,     /* bits not in {3,4}; group_size not 0 or a power
+                                  of two >= 128; batch outside [1,16]            */
+  OWQ_ERR_WEAK_INDEX = 3,      /* weak_idx not strictly ascending, >= c_in,
+                                  n_weak > c_in, or c_in > 65536                 */
+  OWQ_ERR_ZERO_POINT = 4,      /* zero not an integer in [0, 2^bits - 1]        */
+  OWQ_ERR_ZERO_FILL = 5,       /* OWQ_PACK_STRICT and a weak-column code != z  */
+  OWQ_ERR_BUFFER_TOO_SMALL = 6,/* destination / workspace smaller than needed   */
+  OWQ_ERR_BAD_BLOB = 7,        /* header magic/version/shape mismatch           */
+  OWQ_ERR_CUDA = 8,            /* a CUDA runtime call or launch failed          */
+  OWQ_ERR_NCCL = 9,            /* an NCCL call failed                           */
+  OWQ_ERR_CODE_RANGE = 10      /* OWQ_PACK_U8_CODES and a code > 2^bits - 1     */
+} owq_status;
+
+/* Shape of one quantized linear layer (W in R^{C_out x C_in}). */
+typedef struct {
+  int32_t c_out;       /* M: output features (rows)                        */
+  int32_t c_in;        /* K: input features (columns), 1..65536            */
+  int32_t bits;        /* b: 3 or 4                         */
+  int32_t group_size;  /* g: 0 = per output row, else a power of two >= 128 */
+  int32_t n_weak;      /* k: number of fp16 weak columns, 0..c_in          */
+} owq_shape;
+
+/* The paper's representation in host memory ("interchange form"). */
+typedef struct {
+  const uint8_t  *codes;     /* canonical bit stream: row-major, LSB-first,
+                                each row padded to a whole byte; row stride
+                                ceil(c_in*bits/8) bytes  */
+  const uint16_t *scale;     /* fp16 [c_out][G], G = g ? ceil(c_in/g) : 1     */
+  const uint16_t *zero;      /* fp16 [c_out][G], integer-valued codes          */
+  const uint16_t *weak_idx;  /* u16 [n_weak], strictly ascending, < c_in       */
+  const uint16_t *weak_val;  /* fp16 [c_out][n_weak], row-major                */
+} owq_host_layer;
+
+/* owq_pack flags */
+#define OWQ_PACK_STRICT 1    /* reject weak-column codes != z instead of zero-filling */
+#define OWQ_PACK_U8_CODES 2  /* layer->codes is one code per byte, [c_out][c_in]       */
+
+/* Bytes of the device blob for `shape` (header + padded code units + weak
+ * units + scale/zero blocks + weak index list).  0 on an invalid shape. */
+size_t owq_packed_bytes(const owq_shape *shape);
+
+/* Host packer (C++, runs once per layer, off the hot path): validates the
+ * paper representation and writes the device layout into h_blob.  Weak-column
+ * codes are rewritten to that row/group's zero point ("zero-filled", P:114,
+ * reading s10) unless OWQ_PACK_STRICT.  Bit-exact, deterministic. */
+owq_status owq_pack_host(const owq_shape *shape, const owq_host_layer *layer,
+                         int flags, void *h_blob, size_t blob_bytes);
+
+/* owq_pack_host into a temporary host buffer, then a copy to d_packed on
+ * `stream`; returns after the copy completed (packing is offline). */
+owq_status owq_pack(const owq_shape *shape, const owq_host_layer *layer,
+                    int flags, void *d_packed, size_t d_bytes, void *stream);
+
+/* Host inverse of the packer (test hook): recovers shape, one code per byte
+ * [c_out][c_in] (weak columns hold the zero point), fp16 scale/zero [c_out][G],
+ * weak_idx [n_weak], weak_val [c_out][n_weak].  Any output pointer may be NULL. */
+owq_status owq_blob_decode_host(const void *h_blob, size_t blob_bytes,
+                                owq_shape *shape_out, uint8_t *codes,
+                                uint16_t *scale, uint16_t *zero,
+                                uint16_t *weak_idx, uint16_t *weak_val);
+
+/* Device inverse of the code layout (test hook): one code per byte,
+ * d_codes [c_out][c_in] row-major. */
+owq_status owq_unpack_codes(const owq_shape *shape, const void *d_packed,
+                            uint8_t *d_codes, void *stream);
+
+/* Workspace for the split-K (stream-K) reduction of owq_gemv /
+ * owq_gemm_small_batch on the current device: per-row-block arrival counters
+ * plus fp32 partial sums.  The caller zero-fills it ONCE; every call leaves
+ * the counters at zero again.  One workspace must not be used by two calls
+ * that may run concurrently. */
+size_t owq_workspace_bytes(const owq_shape *shape, int batch);
+
+/* y = W_hat x for one activation vector (batch 1).
+ * d_x: fp16 [c_in]; d_y: [c_out], fp32 if y_f32 else fp16 (RNE).
+ * fp32 accumulation of exact (q - z) * x products. */
+owq_status owq_gemv(const owq_shape *shape, const void *d_packed,
+                    const uint16_t *d_x, void *d_y, int y_f32,
+                    void *d_workspace, size_t ws_bytes, void *stream);
+
+/* Y = W_hat X for B in [1, 16] activation rows: d_x fp16 [B][c_in] row-major,
+ * d_y [B][c_out] (fp32 if y_f32).  Same arithmetic as owq_gemv; the tensor-core
+ * B operand carries up to 8 activation rows per mma, 16 with two n-tiles. */
+owq_status owq_gemm_small_batch(const owq_shape *shape, const void *d_packed,
+                                const uint16_t *d_x, int batch, void *d_y,
+                                int y_f32, void *d_workspace, size_t ws_bytes,
+                                void *stream);
+
+/* Test/tuning hook: same as owq_gemm_small_batch with an explicit grid size
+ * (number of CTAs; 0 = one per SM).  Small grids exercise the stream-K
+ * partial-sum path with many pieces per row-block. */
+owq_status owq_gemm_small_batch_grid(const owq_shape *shape, const void *d_packed,
+                                     const uint16_t *d_x, int batch, void *d_y,
+                                     int y_f32, void *d_workspace, size_t ws_bytes,
+                                     int grid, void *stream);
+
+/* ---------------- tensor parallelism over NCCL (one process per GPU) ------- */
+#define OWQ_TP_ROWS 0   /* split c_out: each rank owns a row slice; all-gather y  */
+#define OWQ_TP_COLS 1   /* split c_in: each rank owns a column slice; all-reduce  */
+
+typedef struct owq_tp owq_tp;   /* owns one ncclComm_t */
+
+/* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller
+ * (torch.distributed) before owq_tp_init on every rank. */
+owq_status owq_tp_get_unique_id(void *id128);
+owq_status owq_tp_init(const void *id128, int world, int rank, owq_tp **out);
+owq_status owq_tp_destroy(owq_tp *tp);
+
+/* Slice of `full` owned by `rank` (host only, no GPU needed).  ROWS: rows
+ * [r0, r1) with r0 = round(rank*M/world) to a multiple of 16; every column,
+ * every weak column.  COLS: columns [c0, c1), boundaries at multiples of
+ * max(group_size, 64); weak columns inside the slice, re-based to the slice.
+ * offset_out receives r0 (ROWS) or c0 (COLS). */
+owq_status owq_tp_shard_shape(const owq_shape *full, const owq_host_layer *full_layer,
+                              int mode, int world, int rank,
+                              owq_shape *shard_out, int32_t *offset_out);
+
+/* Pack rank's slice of `full_layer` into h_blob (host, no GPU). */
+owq_status owq_tp_shard_host(const owq_shape *full, const owq_host_layer *full_layer,
+                             int mode, int world, int rank, int flags,
+                             void *h_blob, size_t blob_bytes);
+
+/* owq_tp_shard_host + copy to d_packed_shard on `stream` (blocking). */
+owq_status owq_tp_shard(const owq_shape *full, const owq_host_layer *full_layer,
+                        int mode, int world, int rank, int flags,
+                        void *d_packed_shard, size_t d_bytes, void *stream);
+
+/* Workspace of owq_tp_gemv for this rank (zero-filled once by the caller). */
+size_t owq_tp_workspace_bytes(const owq_shape *full, int mode, int world, int batch);
+
+/* Tensor-parallel Y = W_hat X.  `shard` is this rank's slice shape (from
+ * owq_tp_shard_shape).  ROWS: d_x is the full fp16 [B][c_in] on every rank;
+ * local fused GEMV, then ncclAllGather of the y slices.  COLS: d_x is the
+ * rank's column slice fp16 [B][c1-c0]; local fp32 partial Y (including the
+ * rank's weak columns), then ncclAllReduce(sum, fp32).  d_y: the full
+ * [B][c_out] on every rank (fp32 if y_f32).  Everything is enqueued on `stream`. */
+owq_status owq_tp_gemv(owq_tp *tp, int mode, const owq_shape *full, const owq_shape *shard,
+                       const void *d_packed_shard, const uint16_t *d_x, int batch,
+                       void *d_y, int y_f32, void *d_workspace, size_t ws_bytes,
+                       void *stream);
+
+/* Host-only: [r0, r1) (ROWS) or [c0, c1) (COLS) owned by `rank`. */
+owq_status owq_tp_bounds(const owq_shape *full, int mode, int world, int rank,
+                         int32_t *begin, int32_t *end);
+
+const char *owq_status_string(owq_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OWQ_H_ */

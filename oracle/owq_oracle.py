@@ -40,7 +40,7 @@ __all__ = [
     "quantize", "dequantize", "search_clip", "rtn_delta", "sensitivity",
     "select_weak", "optq_quantize", "owq_quantize", "budget_to_k",
     "effective_bits", "pack_canonical", "unpack_canonical", "dequant_matrix",
-    "matvec", "layer_error", "fp16_bits", "from_fp16_bits",
+    "matvec", "matvec_rows", "layer_error", "fp16_bits", "from_fp16_bits",
 ]
 
 PERCDAMP = 0.01        # reading s2: OPTQ lineage
@@ -402,6 +402,24 @@ def matvec(rep: Rep, x: np.ndarray) -> np.ndarray:
     if rep.k:
         y += x[:, rep.weak_idx] @ rep.weak_val.T
     return y
+
+
+def matvec_rows(rep: Rep, x: np.ndarray, rows) -> np.ndarray:
+    """The same definition as ``matvec`` evaluated for selected output rows only
+    (for sampled parity at sizes where the full fp64 matrix does not fit):
+    y[b, r] for r in rows, one row at a time."""
+    x = np.atleast_2d(np.asarray(x, dtype=np.float64))
+    K = rep.K
+    gi = np.array([j // rep.group if rep.group else 0 for j in range(K)])
+    weak = np.asarray(rep.weak_idx, dtype=np.int64)
+    out = np.zeros((x.shape[0], len(rows)))
+    for n, i in enumerate(rows):
+        low = rep.scale[i, gi] * (rep.codes[i].astype(np.float64) - rep.zero[i, gi])
+        low[weak] = 0.0
+        out[:, n] = x @ low
+        if weak.size:
+            out[:, n] += x[:, weak] @ rep.weak_val[i]
+    return out
 
 
 def layer_error(W, What, X) -> float:

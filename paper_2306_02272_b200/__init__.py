@@ -1,0 +1,377 @@
+"""paper_2306_02272_b200 -- B200-native OWQ (arXiv 2306.02272) hot path.
+
+Thin ctypes binding over ``libowq.so`` (include/owq.h).  Every function here
+only marshals arguments: packing runs in the C++ packer, every step of the
+GEMV runs in the sm_100a kernels.  There is no CPU fallback: importing works
+without a GPU (the library loads), but any device call raises if CUDA or the
+library is unavailable.
+
+Names mirror the C ABI (owq_pack, owq_gemv, owq_gemm_small_batch, owq_tp_gemv,
+...).  Device buffers are torch tensors; the stream is torch's current stream
+unless one is passed.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "OwqError", "Shape", "lib", "canonical_pack", "owq_packed_bytes", "owq_pack_host",
+    "owq_pack", "owq_blob_decode_host", "owq_unpack_codes", "owq_workspace_bytes",
+    "workspace", "owq_gemv", "owq_gemm_small_batch", "owq_gemm_small_batch_grid",
+    "owq_tp_get_unique_id", "owq_tp_init", "owq_tp_destroy", "owq_tp_bounds",
+    "owq_tp_shard_shape", "owq_tp_shard_host", "owq_tp_shard", "owq_tp_workspace_bytes",
+    "owq_tp_gemv", "OwqLinear", "OWQ_TP_ROWS", "OWQ_TP_COLS", "OWQ_PACK_STRICT",
+    "OWQ_PACK_U8_CODES", "EXPORTED_SYMBOLS",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libowq.so")
+
+OWQ_TP_ROWS, OWQ_TP_COLS = 0, 1
+OWQ_PACK_STRICT, OWQ_PACK_U8_CODES = 1, 2
+
+# every symbol include/owq.h declares
+EXPORTED_SYMBOLS = [
+    "owq_packed_bytes", "owq_pack_host", "owq_pack", "owq_blob_decode_host",
+    "owq_unpack_codes", "owq_workspace_bytes", "owq_gemv", "owq_gemm_small_batch",
+    "owq_gemm_small_batch_grid", "owq_tp_get_unique_id", "owq_tp_init", "owq_tp_destroy",
+    "owq_tp_shard_shape", "owq_tp_shard_host", "owq_tp_shard", "owq_tp_workspace_bytes",
+    "owq_tp_gemv", "owq_tp_bounds", "owq_status_string",
+]
+
+
+class OwqError(RuntimeError):
+    pass
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("c_out", ctypes.c_int32), ("c_in", ctypes.c_int32), ("bits", ctypes.c_int32),
+                ("group_size", ctypes.c_int32), ("n_weak", ctypes.c_int32)]
+
+    def __repr__(self):
+        return (f"Shape(c_out={self.c_out}, c_in={self.c_in}, bits={self.bits}, "
+                f"group_size={self.group_size}, n_weak={self.n_weak})")
+
+    def tup(self):
+        return (self.c_out, self.c_in, self.bits, self.group_size, self.n_weak)
+
+
+class _HostLayer(ctypes.Structure):
+    _fields_ = [("codes", ctypes.c_void_p), ("scale", ctypes.c_void_p), ("zero", ctypes.c_void_p),
+                ("weak_idx", ctypes.c_void_p), ("weak_val", ctypes.c_void_p)]
+
+
+_lib = None
+_P = ctypes.c_void_p
+_S = ctypes.POINTER(Shape)
+
+
+def lib():
+    """Load libowq.so (built in-tree by __graft_entry__.build()); fail loudly."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise OwqError(f"{LIB_PATH} is missing: run `python -m paper_2306_02272_b200.build` "
+                       "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    st = ctypes.c_int
+    sz = ctypes.c_size_t
+    sig = {
+        "owq_packed_bytes": (sz, [_S]),
+        "owq_pack_host": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.c_int, _P, sz]),
+        "owq_pack": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.c_int, _P, sz, _P]),
+        "owq_blob_decode_host": (st, [_P, sz, _S, _P, _P, _P, _P, _P]),
+        "owq_unpack_codes": (st, [_S, _P, _P, _P]),
+        "owq_workspace_bytes": (sz, [_S, ctypes.c_int]),
+        "owq_gemv": (st, [_S, _P, _P, _P, ctypes.c_int, _P, sz, _P]),
+        "owq_gemm_small_batch": (st, [_S, _P, _P, ctypes.c_int, _P, ctypes.c_int, _P, sz, _P]),
+        "owq_gemm_small_batch_grid": (st, [_S, _P, _P, ctypes.c_int, _P, ctypes.c_int, _P, sz,
+                                           ctypes.c_int, _P]),
+        "owq_tp_get_unique_id": (st, [_P]),
+        "owq_tp_init": (st, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+        "owq_tp_destroy": (st, [_P]),
+        "owq_tp_bounds": (st, [_S, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                               ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
+        "owq_tp_shard_shape": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.c_int, ctypes.c_int,
+                                    ctypes.c_int, _S, ctypes.POINTER(ctypes.c_int32)]),
+        "owq_tp_shard_host": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int, ctypes.c_int, _P, sz]),
+        "owq_tp_shard": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.c_int, ctypes.c_int,
+                              ctypes.c_int, ctypes.c_int, _P, sz, _P]),
+        "owq_tp_workspace_bytes": (sz, [_S, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+        "owq_tp_gemv": (st, [_P, ctypes.c_int, _S, _S, _P, _P, ctypes.c_int, _P, ctypes.c_int,
+                             _P, sz, _P]),
+        "owq_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(status):
+    if status != 0:
+        raise OwqError(lib().owq_status_string(status).decode())
+
+
+def _shape(s) -> Shape:
+    if isinstance(s, Shape):
+        return s
+    if isinstance(s, dict):
+        return Shape(s["M"], s["K"], s["bits"], s["group"], len(s["weak_idx"]))
+    return Shape(*s)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def canonical_pack(codes: np.ndarray, bits: int) -> np.ndarray:
+    """One code per byte [M][K] -> the paper-side canonical stream (row-major,
+    LSB-first, rows byte-padded)."""
+    codes = np.ascontiguousarray(codes, dtype=np.uint8)
+    M, K = codes.shape
+    planes = ((codes[:, :, None] >> np.arange(bits, dtype=np.uint8)) & 1).reshape(M, K * bits)
+    return np.packbits(planes, axis=1, bitorder="little")
+
+
+@dataclass
+class _HostArrays:
+    layer: _HostLayer
+    keep: tuple
+
+
+def _host_layer(codes, scale, zero, weak_idx, weak_val) -> _HostArrays:
+    arrs = [np.ascontiguousarray(codes, dtype=np.uint8),
+            np.ascontiguousarray(scale, dtype=np.uint16),
+            np.ascontiguousarray(zero, dtype=np.uint16),
+            np.ascontiguousarray(weak_idx, dtype=np.uint16),
+            np.ascontiguousarray(weak_val, dtype=np.uint16)]
+    L = _HostLayer(*[a.ctypes.data if a.size else None for a in arrs])
+    return _HostArrays(L, tuple(arrs))
+
+
+def _layer_from(rep: dict, flags: int):
+    """rep: dict with codes (u8 [M][K] one per byte, or canonical if `canonical`),
+    scale_f16/zero_f16/weak_val_f16 (u16 bit patterns), weak_idx (u16)."""
+    canonical = rep.get("canonical", False)
+    if not canonical:
+        flags |= OWQ_PACK_U8_CODES
+    return _host_layer(rep["codes"], rep["scale_f16"], rep["zero_f16"], rep["weak_idx"],
+                       rep["weak_val_f16"]), flags
+
+
+def owq_packed_bytes(shape) -> int:
+    return int(lib().owq_packed_bytes(ctypes.byref(_shape(shape))))
+
+
+def owq_pack_host(shape, rep: dict, flags: int = 0) -> np.ndarray:
+    s = _shape(shape)
+    n = owq_packed_bytes(s)
+    if n == 0:
+        raise OwqError("OWQ_ERR_UNSUPPORTED")
+    blob = np.empty(n, dtype=np.uint8)
+    hl, flags = _layer_from(rep, flags)
+    _check(lib().owq_pack_host(ctypes.byref(s), ctypes.byref(hl.layer), flags, blob.ctypes.data, n))
+    return blob
+
+
+def owq_pack(shape, rep: dict, flags: int = 0, device=None, stream=None):
+    import torch
+    s = _shape(shape)
+    n = owq_packed_bytes(s)
+    if n == 0:
+        raise OwqError("OWQ_ERR_UNSUPPORTED")
+    d = torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+    hl, flags = _layer_from(rep, flags)
+    _check(lib().owq_pack(ctypes.byref(s), ctypes.byref(hl.layer), flags, d.data_ptr(), n,
+                          _stream(stream)))
+    return d
+
+
+def owq_blob_decode_host(blob: np.ndarray) -> dict:
+    blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    s = Shape()
+    _check(lib().owq_blob_decode_host(blob.ctypes.data, blob.size, ctypes.byref(s),
+                                      None, None, None, None, None))
+    M, K, G = s.c_out, s.c_in, (1 if s.group_size == 0 else -(-s.c_in // s.group_size))
+    out = {"shape": s, "codes": np.zeros((M, K), np.uint8), "scale_f16": np.zeros((M, G), np.uint16),
+           "zero_f16": np.zeros((M, G), np.uint16), "weak_idx": np.zeros(s.n_weak, np.uint16),
+           "weak_val_f16": np.zeros((M, s.n_weak), np.uint16)}
+    _check(lib().owq_blob_decode_host(blob.ctypes.data, blob.size, ctypes.byref(s),
+                                      *[_ptr(out[k]) if out[k].size else None for k in
+                                        ("codes", "scale_f16", "zero_f16", "weak_idx", "weak_val_f16")]))
+    return out
+
+
+def owq_unpack_codes(shape, d_packed, stream=None):
+    import torch
+    s = _shape(shape)
+    out = torch.empty((s.c_out, s.c_in), dtype=torch.uint8, device=d_packed.device)
+    _check(lib().owq_unpack_codes(ctypes.byref(s), d_packed.data_ptr(), out.data_ptr(), _stream(stream)))
+    return out
+
+
+def owq_workspace_bytes(shape, batch: int = 1) -> int:
+    return int(lib().owq_workspace_bytes(ctypes.byref(_shape(shape)), batch))
+
+
+def workspace(shape, batch: int = 1, device=None, grid: int = 0):
+    """Zero-filled workspace (counters stay zero between calls)."""
+    import torch
+    n = owq_workspace_bytes(shape, batch)
+    if grid:
+        n = max(n, n + (grid * batch * 64 * 4))
+    return torch.zeros(max(n, 256), dtype=torch.uint8, device=device or "cuda")
+
+
+def _out(s: Shape, B: int, y, y_f32: bool, device):
+    import torch
+    if y is None:
+        y = torch.empty((B, s.c_out), dtype=torch.float32 if y_f32 else torch.float16, device=device)
+    return y
+
+
+def owq_gemv(shape, d_packed, x, y=None, y_f32=False, ws=None, stream=None):
+    """y = W_hat x for one fp16 vector x [c_in] (or [1][c_in]); returns y [1][c_out]."""
+    s = _shape(shape)
+    y = _out(s, 1, y, y_f32, x.device)
+    ws = ws if ws is not None else workspace(s, 1, x.device)
+    _check(lib().owq_gemv(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), y.data_ptr(),
+                          int(bool(y_f32)), ws.data_ptr(), ws.numel(), _stream(stream)))
+    return y
+
+
+def owq_gemm_small_batch(shape, d_packed, x, y=None, y_f32=False, ws=None, stream=None):
+    """Y = W_hat X for fp16 X [B][c_in], B in [1, 16]; returns Y [B][c_out]."""
+    s = _shape(shape)
+    B = x.shape[0] if x.dim() == 2 else 1
+    y = _out(s, B, y, y_f32, x.device)
+    ws = ws if ws is not None else workspace(s, B, x.device)
+    _check(lib().owq_gemm_small_batch(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B,
+                                      y.data_ptr(), int(bool(y_f32)), ws.data_ptr(), ws.numel(),
+                                      _stream(stream)))
+    return y
+
+
+def owq_gemm_small_batch_grid(shape, d_packed, x, grid: int, y=None, y_f32=False, ws=None, stream=None):
+    s = _shape(shape)
+    B = x.shape[0] if x.dim() == 2 else 1
+    y = _out(s, B, y, y_f32, x.device)
+    ws = ws if ws is not None else workspace(s, B, x.device, grid=grid)
+    _check(lib().owq_gemm_small_batch_grid(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B,
+                                           y.data_ptr(), int(bool(y_f32)), ws.data_ptr(), ws.numel(),
+                                           grid, _stream(stream)))
+    return y
+
+
+# ---------------------------------------------------------------- tensor parallel
+def owq_tp_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().owq_tp_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return buf.raw
+
+
+def owq_tp_init(uid: bytes, world: int, rank: int):
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    h = ctypes.c_void_p()
+    _check(lib().owq_tp_init(ctypes.cast(buf, ctypes.c_void_p), world, rank, ctypes.byref(h)))
+    return h
+
+
+def owq_tp_destroy(h):
+    _check(lib().owq_tp_destroy(h))
+
+
+def owq_tp_bounds(shape, mode: int, world: int, rank: int):
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().owq_tp_bounds(ctypes.byref(_shape(shape)), mode, world, rank, ctypes.byref(a),
+                               ctypes.byref(b)))
+    return a.value, b.value
+
+
+def owq_tp_shard_shape(shape, rep: dict, mode: int, world: int, rank: int):
+    s = _shape(shape)
+    hl, flags = _layer_from(rep, 0)
+    out, off = Shape(), ctypes.c_int32()
+    _check(lib().owq_tp_shard_shape(ctypes.byref(s), ctypes.byref(hl.layer), mode, world, rank,
+                                    ctypes.byref(out), ctypes.byref(off)))
+    return out, off.value
+
+
+def owq_tp_shard_host(shape, rep: dict, mode: int, world: int, rank: int, flags: int = 0):
+    s = _shape(shape)
+    ss, _ = owq_tp_shard_shape(s, rep, mode, world, rank)
+    n = owq_packed_bytes(ss)
+    blob = np.empty(n, np.uint8)
+    hl, flags = _layer_from(rep, flags)
+    _check(lib().owq_tp_shard_host(ctypes.byref(s), ctypes.byref(hl.layer), mode, world, rank, flags,
+                                   blob.ctypes.data, n))
+    return ss, blob
+
+
+def owq_tp_shard(shape, rep: dict, mode: int, world: int, rank: int, flags: int = 0, device=None,
+                 stream=None):
+    import torch
+    s = _shape(shape)
+    ss, _ = owq_tp_shard_shape(s, rep, mode, world, rank)
+    n = owq_packed_bytes(ss)
+    d = torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+    hl, flags = _layer_from(rep, flags)
+    _check(lib().owq_tp_shard(ctypes.byref(s), ctypes.byref(hl.layer), mode, world, rank, flags,
+                              d.data_ptr(), n, _stream(stream)))
+    return ss, d
+
+
+def owq_tp_workspace_bytes(shape, mode: int, world: int, batch: int = 1) -> int:
+    return int(lib().owq_tp_workspace_bytes(ctypes.byref(_shape(shape)), mode, world, batch))
+
+
+def owq_tp_gemv(tp, mode, full, shard, d_packed, x, y, y_f32=False, ws=None, stream=None):
+    f, s = _shape(full), _shape(shard)
+    B = x.shape[0] if x.dim() == 2 else 1
+    _check(lib().owq_tp_gemv(tp, mode, ctypes.byref(f), ctypes.byref(s), d_packed.data_ptr(),
+                             x.data_ptr(), B, y.data_ptr(), int(bool(y_f32)), ws.data_ptr(),
+                             ws.numel(), _stream(stream)))
+    return y
+
+
+class OwqLinear:
+    """A packed OWQ layer resident in HBM: ``y = layer(x)`` (x fp16 [B][c_in])."""
+
+    def __init__(self, rep: dict, device=None, max_batch: int = 16, flags: int = 0):
+        import torch
+        self.shape = _shape((rep["M"], rep["K"], rep["bits"], rep["group"], len(rep["weak_idx"])))
+        self.device = torch.device(device or "cuda")
+        self.packed = owq_pack(self.shape, rep, flags, device=self.device)
+        self.ws = workspace(self.shape, max_batch, self.device)
+
+    @property
+    def nbytes(self) -> int:
+        return self.packed.numel()
+
+    def __call__(self, x, y=None, y_f32=False, stream=None):
+        if x.dim() == 1:
+            x = x.unsqueeze(0)
+        return owq_gemm_small_batch(self.shape, self.packed, x, y=y, y_f32=y_f32, ws=self.ws,
+                                    stream=stream)

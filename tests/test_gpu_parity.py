@@ -1,0 +1,195 @@
+"""GPU parity of the CUDA path (through the C-ABI) against the CPU oracle.
+
+Tolerance (BASELINE.json north_star): relative error <= 2e-3 per output element
+(fp32 accumulation vs the fp64 oracle), with the near-zero floor of DESIGN.md
+reading s16.  Packing, unpacking and index work are bit-exact; probes with a
+closed-form answer are bit-exact too.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from owq_testutil import TOL, rel_err, rep_from_synth, synth_from_rep
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2306_02272_b200 as owq  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    return torch.device("cuda:0")
+
+
+def run(d, x_np, dev, y_f32=True, grid=0):
+    layer = owq.OwqLinear(d, device=dev)
+    x = torch.from_numpy(np.ascontiguousarray(x_np, np.float16)).to(dev)
+    if grid:
+        y = owq.owq_gemm_small_batch_grid(layer.shape, layer.packed, x, grid, y_f32=y_f32)
+    else:
+        y = layer(x, y_f32=y_f32)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy().astype(np.float64), layer
+
+
+SHAPES = [
+    # (M, K, bits, group, k)             what it covers
+    (768, 768, 3, 0, 8),                 # BASELINE config 1
+    (100, 200, 3, 0, 5),                 # ragged rows / columns / k tail
+    (64, 64, 3, 0, 0),                   # one super-step, no weak columns
+    (1, 1, 3, 0, 1),                     # degenerate: one weight, weak
+    (130, 1100, 4, 128, 9),              # 4-bit g128, partial last group
+    (4096, 4096, 3, 0, 5),               # OPT-6.7B qkvo
+    (512, 2048, 4, 1024, 3),             # g1024
+    (192, 3000, 3, 0, 153),              # many weak columns (3.1-bit style), 10 full chunks + tail
+    (64, 5000, 3, 0, 136),               # two weak units
+]
+
+
+@pytest.mark.parametrize("M,K,bits,group,k", SHAPES)
+def test_gemv_parity_vs_oracle(dev, M, K, bits, group, k):
+    d = synth.representation(M, K, bits, group, k, seed=M * 7 + K)
+    rep = rep_from_synth(d)
+    x = synth.activations(1, K, seed=K, outliers=d["weak_idx"][:8])
+    y, _ = run(d, x, dev)
+    y_ref = O.matvec(rep, x.astype(np.float64))
+    e, eu = rel_err(y, y_ref)
+    assert e <= TOL, (e, eu)
+
+
+@pytest.mark.parametrize("B", [2, 3, 8, 9, 16])
+@pytest.mark.parametrize("M,K,bits,group,k", [(256, 1024, 4, 128, 4), (300, 700, 3, 0, 11)])
+def test_small_batch_parity(dev, B, M, K, bits, group, k):
+    d = synth.representation(M, K, bits, group, k, seed=B + M)
+    rep = rep_from_synth(d)
+    x = synth.activations(B, K, seed=B * 3, outliers=d["weak_idx"])
+    y, _ = run(d, x, dev)
+    y_ref = O.matvec(rep, x.astype(np.float64))
+    assert y.shape == (B, M)
+    e, _ = rel_err(y, y_ref)
+    assert e <= TOL
+
+
+def test_fp16_output(dev):
+    d = synth.representation(333, 1500, 3, 0, 7, seed=5)
+    x = synth.activations(4, 1500, seed=6, outliers=d["weak_idx"])
+    y16, _ = run(d, x, dev, y_f32=False)
+    y_ref = O.matvec(rep_from_synth(d), x.astype(np.float64))
+    e, _ = rel_err(y16, y_ref)
+    assert e <= TOL
+
+
+def test_oracle_quantizer_output_config1(dev):
+    # BASELINE config 1 end to end: OWQ quantization by the oracle (768x768, k=8),
+    # then the GPU hot path on the oracle's representation.
+    W, X, ch = synth.weights_and_calib(768, 768, N=2048, n_outliers=8, seed=2306)
+    rep = O.owq_quantize(W, X, 3, 8)
+    d = synth_from_rep(rep)
+    x = synth.activations(1, 768, seed=2307, outliers=ch)
+    y, layer = run(d, x, dev)
+    e, _ = rel_err(y, O.matvec(rep, x.astype(np.float64)))
+    assert e <= TOL
+    # strict packing accepts it (codes of weak columns already equal z)
+    owq.owq_pack(layer.shape, d, flags=owq.OWQ_PACK_STRICT, device=dev)
+
+
+@pytest.mark.parametrize("bits,group", [(3, 0), (4, 128)])
+def test_device_unpack_bit_exact(dev, bits, group):
+    M, K, k = 200, 1500, 6
+    d = synth.representation(M, K, bits, group, k, seed=9)
+    shape = owq.Shape(M, K, bits, group, k)
+    packed = owq.owq_pack(shape, d, device=dev)
+    codes = owq.owq_unpack_codes(shape, packed).cpu().numpy()
+    expect = d["codes"].copy()
+    z = O.from_fp16_bits(d["zero_f16"]).astype(np.uint8)
+    for j in d["weak_idx"]:
+        expect[:, j] = z[:, j // group if group else 0]
+    assert np.array_equal(codes, expect)
+
+
+@pytest.mark.parametrize("bits,group", [(3, 0), (4, 128)])
+def test_probes_bit_exact(dev, bits, group):
+    # x = e_j: weak j -> y = v[:, t] exactly; non-weak j -> y_i = s_i (q_ij - z_i) exactly
+    # (fp16 s times an integer <= 15 is exact in fp32).  Covers index, layout, zero fill.
+    M, K, k = 130, 600, 5
+    d = synth.representation(M, K, bits, group, k, seed=11)
+    rep = rep_from_synth(d)
+    layer = owq.OwqLinear(d, device=dev)
+    js = list(d["weak_idx"]) + [0, 1, 63, 64, 127, 128, 300, 599]
+    X = np.zeros((len(js), K), np.float16)
+    for n, j in enumerate(js):
+        X[n, j] = 1.0
+    for a in range(0, len(js), 16):
+        xb = torch.from_numpy(X[a:a + 16]).to(dev)
+        y = layer(xb, y_f32=True).cpu().numpy().astype(np.float64)
+        y_ref = O.matvec(rep, X[a:a + 16].astype(np.float64))
+        assert np.array_equal(y, y_ref)
+
+
+@pytest.mark.parametrize("grid", [1, 2, 3, 7, 13, 64, 500])
+def test_stream_k_any_grid_and_deterministic(dev, grid):
+    M, K, bits, group, k = 700, 5000, 3, 0, 20
+    d = synth.representation(M, K, bits, group, k, seed=grid)
+    rep = rep_from_synth(d)
+    x = synth.activations(2, K, seed=3, outliers=d["weak_idx"])
+    y1, layer = run(d, x, dev, grid=grid)
+    e, _ = rel_err(y1, O.matvec(rep, x.astype(np.float64)))
+    assert e <= TOL
+    xt = torch.from_numpy(x).to(dev)
+    for _ in range(3):     # counters reset to 0 after every call; results bit-identical
+        y2 = owq.owq_gemm_small_batch_grid(layer.shape, layer.packed, xt, grid, y_f32=True)
+        assert np.array_equal(y2.cpu().numpy().astype(np.float64), y1)
+
+
+@pytest.mark.parametrize("M,K,k", [(12288, 12288, 15), (49152, 12288, 3), (12288, 49152, 15)])
+def test_full_size_opt175b_sampled(dev, M, K, k):
+    # BASELINE config 5 at full size in the bench launch configuration; the oracle
+    # computes a sample of rows one by one (every row-block boundary class covered).
+    d = synth.representation(M, K, 3, 0, k, seed=M + K)
+    rep = rep_from_synth(d)
+    x = synth.activations(1, K, seed=1, outliers=d["weak_idx"][:8])
+    y, _ = run(d, x, dev)
+    r = np.random.default_rng(0)
+    rows = sorted(set([0, 1, 63, 64, M - 1, M - 64] + list(r.choice(M, 120, replace=False))))
+    y_ref = O.matvec_rows(rep, x.astype(np.float64), rows)
+    e, _ = rel_err(y[:, rows], y_ref)
+    assert e <= TOL
+    # a property that holds at any size: sum_i y_i = sum_j x_j * colsum_j(W_hat) -- skipped;
+    # row-sample parity above is exact per element.
+
+
+def test_tp_world1_nccl(dev):
+    # NCCL communicator of one rank: both TP modes reproduce the single-GPU result.
+    M, K, bits, group, k = 512, 2048, 4, 128, 6
+    d = synth.representation(M, K, bits, group, k, seed=21)
+    shape = owq.Shape(M, K, bits, group, k)
+    x = synth.activations(2, K, seed=22, outliers=d["weak_idx"])
+    xt = torch.from_numpy(x).to(dev)
+    y_ref = O.matvec(rep_from_synth(d), x.astype(np.float64))
+    tp = owq.owq_tp_init(owq.owq_tp_get_unique_id(), 1, 0)
+    try:
+        for mode in (owq.OWQ_TP_ROWS, owq.OWQ_TP_COLS):
+            ss, packed = owq.owq_tp_shard(shape, d, mode, 1, 0, device=dev)
+            ws = torch.zeros(owq.owq_tp_workspace_bytes(shape, mode, 1, 2), dtype=torch.uint8, device=dev)
+            y = torch.empty((2, M), dtype=torch.float32, device=dev)
+            owq.owq_tp_gemv(tp, mode, shape, ss, packed, xt, y, y_f32=True, ws=ws)
+            torch.cuda.synchronize()
+            e, _ = rel_err(y.cpu().numpy(), y_ref)
+            assert e <= TOL
+    finally:
+        owq.owq_tp_destroy(tp)
+
+
+def test_errors_are_loud(dev):
+    d = synth.representation(64, 128, 3, 0, 2, seed=1)
+    layer = owq.OwqLinear(d, device=dev)
+    x = torch.zeros((17, 128), dtype=torch.float16, device=dev)
+    with pytest.raises(owq.OwqError, match="UNSUPPORTED"):
+        owq.owq_gemm_small_batch(layer.shape, layer.packed, x)
+    wrong = owq.Shape(64, 128, 3, 0, 3)
+    with pytest.raises(owq.OwqError, match="BAD_BLOB"):
+        owq.owq_gemv(wrong, layer.packed, x[0])

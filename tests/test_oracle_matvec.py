@@ -75,3 +75,18 @@ def test_quantizer_output_feeds_matvec():
     # the mixed representation approximates W x far better than zero
     err = np.abs(O.matvec(rep, x) - x @ W.T).max()
     assert err < 0.25 * np.abs(x @ W.T).max()
+
+
+def test_matvec_rows_brute_force():
+    rep = _rep_from_synth(synth.representation(9, 30, 3, 0, 4, seed=21))
+    x = synth.activations(2, 30, seed=22).astype(np.float64)
+    rows = [0, 4, 8]
+    y = O.matvec_rows(rep, x, rows)
+    weak = {int(j): t for t, j in enumerate(rep.weak_idx)}
+    for b in range(2):
+        for n, i in enumerate(rows):
+            acc = 0.0
+            for j in range(30):
+                acc += (rep.weak_val[i, weak[j]] if j in weak else
+                        rep.scale[i, 0] * (int(rep.codes[i, j]) - rep.zero[i, 0])) * x[b, j]
+            assert y[b, n] == pytest.approx(acc, rel=1e-13, abs=1e-15)
