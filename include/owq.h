@@ -38,15 +38,14 @@
  * Device layout (the "packed blob", produced only by owq_pack / owq_pack_host;
  * version OWQ_LAYOUT_VERSION, self-describing: a 256-byte header repeats the
  * shape, so every call re-checks shape agreement).  Rows are grouped in
- * row-blocks of 64 (the last one padded); columns in super-steps of 64 (the
- * last one padded).  Per row-block the record holds its super-steps followed
- * by its weak-column chunks (8 columns each, mma-fragment order; the ragged
- * last chunk row-major, unpadded), so any run of items is one contiguous TMA
- * bulk copy.
- * Inside a super-step, codes are ordered for the mma.sync m16n8k16 A-fragment
- * of each lane and pre-positioned inside 32-bit words so that one LOP3 with an
- * fp16 exponent "magic" yields two exact values 1024 + q*2^p.
- * gives the exact bit map; owq_unpack_codes / owq_blob_decode_host invert it.
+ * row-blocks of 128 (one tcgen05 M=128 tile; the last one padded); columns in
+ * super-steps of 64 (the last one padded).  Per row-block the record holds
+ * its super-steps followed by its weak-column chunks (8 columns each; the
+ * ragged last chunk unpadded), so any run of items is one contiguous TMA bulk
+ * copy.  Inside a super-step each row's 64 codes are 6 (3-bit) or 8 (4-bit)
+ * 32-bit words, pre-positioned so that one LOP3 with an fp16 exponent "magic"
+ * yields two exact values 1024 + q*2^p.  DESIGN.md §5 gives the exact bit map;
+ * owq_unpack_codes / owq_blob_decode_host invert it.
  */
 #ifndef OWQ_H_
 #define OWQ_H_
@@ -58,7 +57,7 @@
 extern "C" {
 #endif
 
-#define OWQ_LAYOUT_VERSION 1
+#define OWQ_LAYOUT_VERSION 2
 #define OWQ_MAX_BATCH 16
 
 typedef enum {

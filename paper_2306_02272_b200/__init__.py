@@ -240,8 +240,8 @@ def workspace(shape, batch: int = 1, device=None, grid: int = 0):
     """Zero-filled workspace (counters stay zero between calls)."""
     import torch
     n = owq_workspace_bytes(shape, batch)
-    if grid:
-        n = max(n, n + (grid * batch * 64 * 4))
+    if grid:   # stream-K partial slots for a non-default grid: grid x batch x 128 rows x f32
+        n = n + grid * batch * 128 * 4
     return torch.zeros(max(n, 256), dtype=torch.uint8, device=device or "cuda")
 
 

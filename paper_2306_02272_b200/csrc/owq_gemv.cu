@@ -1,28 +1,33 @@
-// owq_gemv.cu -- sm_100a kernels of the OWQ hot path (arXiv 2306.02272, P:114,
-// P:276): y = (zero-filled b-bit matrix) x + (fp16 weak columns) x[idx], fused
-// in one launch.
+// owq_gemv.cu -- sm_100a kernel of the OWQ hot path (arXiv 2306.02272, P:114,
+// P:276): y = (zero-filled b-bit matrix) x + (fp16 weak columns) x[idx], one
+// fused launch, batch 1..16.
 //
-// One CTA per SM (persistent, stream-K over "units" of 64 rows x 1024 columns):
-//   warp 8 (producer)  : one elected lane streams units HBM -> a ring of shared
-//                        memory stages with cp.async.bulk (TMA, 1-D) + mbarriers.
-//   warps 0-7 (consume): per unit, warp w decodes 2 super-steps (64 rows x 128
-//                        columns).  Codes -> exact fp16 (q - z) with one LOP3
-//                        ("magic" exponent 0x6400) + one HFMA2 per two weights,
-//                        then mma.sync m16n8k16 (fp32 accumulate) against x
-//                        (the mma B operand carries up to 8 activation rows).
-//                        The scale s is applied in fp32 after accumulation, per
-//                        row (g = 0) or per group (g % 128 == 0).
-//   weak units         : fp16 weak values x gathered x[idx] with mma m16n8k8,
-//                        added after scaling (the paper's separate dense fp16
-//                        GEMV, folded into the same pass).
-//   epilogue           : cross-warp reduction in shared memory; a row-block whose
-//                        units span several CTAs is combined through a
-//                        fp32 workspace by the last-arriving CTA, in a fixed
-//                        order (deterministic).
+// Persistent CTA per SM, byte-balanced stream-K over "items" (a super-step =
+// 128 rows x 64 columns of codes, or a chunk of 8 weak columns).  Warp roles:
+//   producer (1 warp)   : one lane streams stages (runs of items + the matching
+//                         x columns + scale/zero blocks) HBM -> a shared-memory
+//                         ring with cp.async.bulk (TMA) and mbarriers.
+//   decode (DWG x 4)    : one thread per output row.  Codes -> exact fp16 (q - z)
+//                         pairs with one LOP3 ("magic" exponent 0x6400) + one
+//                         HFMA2 per two weights, written to a TMEM A-buffer with
+//                         tcgen05.st; x is re-laid into UMMA core matrices.
+//   MMA (1 warp per WG) : one lane issues tcgen05.mma kind::f16 M=128 N=16 K=16
+//                         (A from TMEM, B = x from shared memory, D fp32 in TMEM;
+//                         one D per warpgroup and scale group, ping-pong) and
+//                         tcgen05.commit -> mbarriers.  MMAs from several issuing
+//                         warps overlap; one issuer serialises at ~46 cycles per
+//                         instruction (tools/umma_tput.cu).
+//   epilogue (4 warps)  : reads D (tcgen05.ld), applies the fp32 scale of the
+//                         row/group, adds the fp16 weak columns x gathered
+//                         x[idx] on CUDA cores (the paper's separate dense fp16
+//                         GEMV, folded in), and writes y -- directly, or
+//                         through the stream-K fixup (last-arriving CTA sums the
+//                         pieces in a fixed order: deterministic).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -33,6 +38,10 @@
 
 namespace owq {
 
+constexpr int kMmaN = 16;                        // tcgen05 N (batch padded to 16)
+constexpr int kXcBytes = 8 * 2 * 128;            // x tile of one super-step in UMMA core matrices
+constexpr uint32_t kFp16Magic = 0x64006400u;     // fp16x2 (1024, 1024)
+
 struct Params {
   const uint8_t* blob;
   const __half* x;
@@ -42,33 +51,25 @@ struct Params {
   Geo g;
   int32_t B;
   int32_t y_f32;
-  int32_t nst;          // pipeline stages
-  int64_t xK;           // row stride of x in elements (K, or the padded copy's stride)
-  int32_t group_log2;   // log2(group_size / 64) (group_size a power of two >= 128)
-  unsigned long long* trace;   // perf experiments only (OWQ_TRACE): per-CTA globaltimer stamps
-  struct {
-    int32_t code_bytes, xstride, x_bytes, sz_blocks, bytes;
-  } sg;
+  int32_t nst;            // pipeline stages
+  int32_t cap;            // items per stage
+  int32_t code_bytes;     // stage region for codes / weak chunks
+  int32_t xraw_stride;    // bytes per raw x row in a stage (cap * 64 * 2)
+  int32_t sz_off;         // scale/zero blocks inside a stage
+  int32_t stage_bytes;
+  int64_t xK;             // row stride of x in elements
+  int32_t group_log2;     // log2(group_size / 64)
+  unsigned long long* trace;   // experiments only (OWQ_TRACE)
+  int32_t dbg;            // experiments only (OWQ_DEBUG): 1 no decode, 2 no TMEM store, 3 no MMA
 };
 
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-// trace slots per CTA (OWQ_TRACE experiments): 0 start, 50/56 last finalize in/out, 62 end
-
-
 // ---------------------------------------------------------------- PTX helpers
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -77,13 +78,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, 0x989680;\n\t"   // suspend-time hint: sleep, don't spin
       "@!P bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t policy) {
+// wait with cycle accounting into a shared counter (trace/experiment mode only)
+__device__ __forceinline__ void mbar_wait_p(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
+  if (acc) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    if ((threadIdx.x & 31) == 0) atomicAdd(acc, (unsigned long long)(clock64() - t0));
+  } else {
+    mbar_wait(bar, parity);
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_addr(dst)),
@@ -95,32 +105,31 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ uint4 ldg_nc128(const void* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
 }
-__device__ __forceinline__ void named_sync_n(int threads) {  // consumer warps only (barrier 1)
-  asm volatile("bar.sync 1, %0;" ::"r"(threads) : "memory");
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
 }
-// D = A(16x16 f16, row) * B(16x8 f16, col) + D, fp32 accumulate
-__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
-__device__ __forceinline__ void mma1688(float* d, uint32_t a0, uint32_t a1, uint32_t b0) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k8.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(b0));
+__device__ __forceinline__ void named_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 __device__ __forceinline__ uint32_t hfma2u(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -129,11 +138,53 @@ __device__ __forceinline__ uint32_t hfma2u(uint32_t a, uint32_t b, uint32_t c) {
 }
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
-constexpr uint32_t kFp16Magic = 0x64006400u;   // fp16x2 (1024, 1024)
+// tcgen05 (5th-gen tensor core + TMEM)
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_t, uint32_t a_t, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_t),
+      "r"(a_t), "l"(b_desc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* d) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+        "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// UMMA shared-memory descriptor, K-major, no swizzle (SM100 version = 1)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// instruction descriptor: D f32, A/B f16, K-major, N = 16, M = 128
+constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kMmaN >> 3) << 17) | ((uint32_t)(kRowBlock >> 4) << 24);
 
-// (w & mask) | magic in ONE LOP3 (magic held in a register: LOP3 has a single
-// immediate slot, and the compiler otherwise emits two LOP3s).
+// (w & MASK) | magic in ONE LOP3 (magic held in a register)
 template <uint32_t MASK>
 __device__ __forceinline__ uint32_t ext(uint32_t w, uint32_t magic) {
   uint32_t d;
@@ -141,47 +192,52 @@ __device__ __forceinline__ uint32_t ext(uint32_t w, uint32_t magic) {
   return d;
 }
 
-// Exact decode of one 3-bit packet (3 words -> 16 fp16x2 of 1024 + q*2^p).
-// Pair P's field is at p = 3*(P%3) (P<9), 3*((P-9)%2) after >>9 (P<15), and
-// P=15 gathers bit 15 / 31 of the three words into p = 6 (owq_layout.h).
-__device__ __forceinline__ void decode3(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t mg, uint32_t* e) {
-  constexpr uint32_t m0 = 0x00070007u, m3 = 0x00380038u, m6 = 0x01C001C0u, ml = 0x00400040u;
-  e[0] = ext<m0>(w0, mg); e[1] = ext<m3>(w0, mg); e[2] = ext<m6>(w0, mg);
-  e[3] = ext<m0>(w1, mg); e[4] = ext<m3>(w1, mg); e[5] = ext<m6>(w1, mg);
-  e[6] = ext<m0>(w2, mg); e[7] = ext<m3>(w2, mg); e[8] = ext<m6>(w2, mg);
-  const uint32_t v0 = w0 >> 9, v1 = w1 >> 9, v2 = w2 >> 9;
-  e[9] = ext<m0>(v0, mg);  e[10] = ext<m3>(v0, mg);
-  e[11] = ext<m0>(v1, mg); e[12] = ext<m3>(v1, mg);
-  e[13] = ext<m0>(v2, mg); e[14] = ext<m3>(v2, mg);
-  e[15] = ext<ml>(v0, mg) + ((v1 & ml) << 1) + ((v2 & ml) << 2);
-}
-// p-index (0: p=0, 1: p=3, 2: p=6) of pair P for 3-bit.
-__host__ __device__ constexpr int pidx3(int P) { return P < 9 ? P % 3 : (P < 15 ? (P - 9) % 2 : 2); }
-
-// 4-bit packet: word i holds pairs 4i..4i+3 at p = 0, 4 (direct) and 0, 4 after >>8.
-__device__ __forceinline__ void decode4(const uint32_t* w, uint32_t mg, uint32_t* e) {
-  constexpr uint32_t m0 = 0x000F000Fu, m4 = 0x00F000F0u;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t v = w[i] >> 8;
-    e[4 * i + 0] = ext<m0>(w[i], mg);
-    e[4 * i + 1] = ext<m4>(w[i], mg);
-    e[4 * i + 2] = ext<m0>(v, mg);
-    e[4 * i + 3] = ext<m4>(v, mg);
-  }
-}
-
+// Decode of one row's super-step (64 codes) into 32 fp16x2 exact (q - z) pairs.
+// 3-bit: pair j < 30 sits in word j/5 at bit 3*(j%5) (sub 0..2) or, after >> 9,
+// at 3*(j%5 - 3); pairs 30/31 gather bit 15/31 of words 0..2 / 3..5 (owq_layout.h).
 template <int BITS>
-struct Dec {
-  static constexpr int NP = BITS == 3 ? 3 : 2;   // distinct field positions
-  __device__ static __forceinline__ int pidx(int P) { return BITS == 3 ? pidx3(P) : (P & 1); }
-  __device__ static __forceinline__ uint32_t mul(int pi) {  // fp16x2 2^-p
-    if (BITS == 3) return pi == 0 ? 0x3C003C00u : (pi == 1 ? 0x30003000u : 0x24002400u);  // 1, 1/8, 1/64
-    return pi == 0 ? 0x3C003C00u : 0x2C002C00u;                                           // 1, 1/16
+struct Decoder {
+  static constexpr int NP = BITS == 3 ? 3 : 2;       // distinct field positions p
+  // HFMA2 multiplier 2^-p and base 1024*2^-p for position index q
+  static __device__ __forceinline__ uint32_t mul(int q) {
+    if (BITS == 3) return q == 0 ? 0x3C003C00u : (q == 1 ? 0x30003000u : 0x24002400u);   // 1, 1/8, 1/64
+    return q == 0 ? 0x3C003C00u : 0x2C002C00u;                                          // 1, 1/16
   }
-  __device__ static __forceinline__ uint32_t base(int pi) {  // fp16x2 1024 * 2^-p
-    if (BITS == 3) return pi == 0 ? 0x64006400u : (pi == 1 ? 0x58005800u : 0x4C004C00u);  // 1024,128,16
-    return pi == 0 ? 0x64006400u : 0x54005400u;                                           // 1024, 64
+  static __device__ __forceinline__ uint32_t base(int q) {
+    if (BITS == 3) return q == 0 ? 0x64006400u : (q == 1 ? 0x58005800u : 0x4C004C00u);   // 1024, 128, 16
+    return q == 0 ? 0x64006400u : 0x54005400u;                                          // 1024, 64
+  }
+  static __device__ __forceinline__ constexpr int pidx(int j) {
+    return BITS == 3 ? (j < 30 ? ((j % 5) < 3 ? (j % 5) : (j % 5) - 3) : 2) : ((j & 3) & 1);
+  }
+  static __device__ __forceinline__ void run(const uint32_t* w, uint32_t mg, const uint32_t* cz, uint32_t* e) {
+    if (BITS == 3) {
+      constexpr uint32_t m0 = 0x00070007u, m3 = 0x00380038u, m6 = 0x01C001C0u, ml = 0x00400040u;
+      uint32_t v[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        v[i] = w[i] >> 9;
+        e[5 * i + 0] = ext<m0>(w[i], mg);
+        e[5 * i + 1] = ext<m3>(w[i], mg);
+        e[5 * i + 2] = ext<m6>(w[i], mg);
+        e[5 * i + 3] = ext<m0>(v[i], mg);
+        e[5 * i + 4] = ext<m3>(v[i], mg);
+      }
+      e[30] = ext<ml>(v[0], mg) + ((v[1] & ml) << 1) + ((v[2] & ml) << 2);
+      e[31] = ext<ml>(v[3], mg) + ((v[4] & ml) << 1) + ((v[5] & ml) << 2);
+    } else {
+      constexpr uint32_t m0 = 0x000F000Fu, m4 = 0x00F000F0u;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t v = w[i] >> 8;
+        e[4 * i + 0] = ext<m0>(w[i], mg);
+        e[4 * i + 1] = ext<m4>(w[i], mg);
+        e[4 * i + 2] = ext<m0>(v, mg);
+        e[4 * i + 3] = ext<m4>(v, mg);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) e[j] = hfma2u(e[j], mul(pidx(j)), cz[pidx(j)]);   // exact q - z
   }
 };
 
@@ -195,57 +251,170 @@ __global__ void owq_pad_x_kernel(const __half* __restrict__ x, __half* __restric
   }
 }
 
-// Stage layout in shared memory (one TMA transaction group per stage):
-//   [codes or weak chunks: cap items][x: B rows x xstride bytes][sz blocks]
-// x and the scale/zero blocks ride in the same stage as the codes, so the
-// consumer loop issues no global loads (their latency explodes while the TMA
-// stream saturates HBM).
-//   code_bytes = cap * max(ss_bytes, weak chunk bytes); xstride = cap*64*2 + 16
-//   (bank skew between batch rows); sz_blocks = max scale/zero blocks per stage.
+// group of code item li (row-block relative super-step index)
+__device__ __forceinline__ int group_of(const Params& p, int li) { return p.g.group ? (li >> p.group_log2) : 0; }
 
-// CTA smem: ring [nst][stage] | red [NW][4][32][4*NB] f32 | xw [B][kpad] f16 | bars
-template <int BITS, int NB, int NW, int IPW>
-__global__ void __launch_bounds__((NW + 1) * 32) __maxnreg__(NW >= 15 ? 128 : 224) owq_gemv_kernel(const Params p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+template <int BITS, int DWG, bool X1>
+struct Cfg {
+  static constexpr int kDecodeWarps = 4 * DWG;            // DWG decode warpgroups
+  static constexpr int kEpiWarp0 = kDecodeWarps;          // 4 epilogue warps (warp % 4 = TMEM lane quarter)
+  static constexpr int kMmaWarp0 = kEpiWarp0 + 4;         // one MMA-issuer warp per warpgroup
+  static constexpr int kProdWarp = kMmaWarp0 + DWG;
+  static constexpr int kWarps = kProdWarp + 1;
+  static constexpr int kThreads = kWarps * 32;
+  static constexpr int kIPB = 2;                          // super-steps per A buffer (one publish)
+  static constexpr int kTmemCols = 512;                   // A: DWG*2*kIPB*32, D: DWG*2*16
+  static constexpr int kACols = kIPB * 32;
+  static constexpr int kDCol0 = DWG * 2 * kACols;
+  // per stage: decode + epilogue warps arrive; with X1 each MMA warp also commits
+  // (its MMAs read x from the stage)
+  static constexpr int kEmptyCount = kDecodeWarps + 4 + (X1 ? DWG : 0);
+};
+
+// Segments of a code stage: maximal runs of items of one scale group.  For
+// per-row scales a stage is one segment.  `ends` = the segment's group has no
+// further item in this CTA's sequence (the next item is in another group or
+// row-block, a weak chunk, or absent).
+struct Seg {
+  int pa, pb, gi;
+  bool ends;
+};
+__device__ __forceinline__ Seg segment(const Params& p, int pa, int cn, int cli, int64_t crb, int nn, int64_t nrb,
+                                       int nli) {
+  Seg sg;
+  sg.pa = pa;
+  sg.gi = group_of(p, cli + pa);
+  if (p.g.group) {
+    const int gend = ((sg.gi + 1) << p.group_log2) - cli - 1;   // last stage position of this group
+    sg.pb = gend < cn - 1 ? gend : cn - 1;
+  } else {
+    sg.pb = cn - 1;
+  }
+  if (sg.pb + 1 < cn) sg.ends = true;
+  else sg.ends = !(nn > 0 && nrb == crb && nli < p.g.nss && group_of(p, nli) == sg.gi);
+  return sg;
+}
+// contiguous share of a stage's n items owned by warpgroup w: [lo, hi)
+__device__ __forceinline__ void share(int n, int w, int dwg, int& lo, int& hi) {
+  const int per = (n + dwg - 1) / dwg;
+  lo = w * per;
+  hi = lo + per < n ? lo + per : n;
+  if (lo > n) lo = n;
+}
+
+template <int BITS, int DWG, bool X1>
+__global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kernel(const Params p) {
+  using C = Cfg<BITS, DWG, X1>;
+  extern __shared__ __align__(1024) uint8_t smem[];
   const Geo& g = p.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gq = lane >> 2, tq = lane & 3;
   const int NST = p.nst;
-  constexpr int CAP = NW * IPW;                       // items per stage
-  constexpr int RED_PER_WARP = 4 * 32 * 4 * NB;       // floats
-  const auto sg = p.sg;
   uint8_t* ring = smem;
-  float* red = reinterpret_cast<float*>(smem + (size_t)NST * sg.bytes);
-  __half* xw = reinterpret_cast<__half*>(red + NW * RED_PER_WARP);
-  uint64_t* full = reinterpret_cast<uint64_t*>(xw + (((size_t)p.B * g.kpad + 7) & ~(size_t)7));
+  uint8_t* xc = smem + (size_t)NST * p.stage_bytes;                      // [DWG][2][kIPB][kXcBytes]
+  __half* xw = reinterpret_cast<__half*>(xc + DWG * 2 * C::kIPB * kXcBytes);   // [B][kpad]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(xw + (((size_t)p.B * g.kpad + 7) & ~(size_t)7));
+  uint64_t* full = bars;
   uint64_t* empty = full + NST;
-  int* flag = reinterpret_cast<int*>(empty + NST);
+  uint64_t* afull = empty + NST;       // [DWG][2]  A buffer + x tile written (4 warps)
+  uint64_t* aempty = afull + 2 * DWG;  // [DWG][2]  MMA done reading them
+  uint64_t* dfull = aempty + 2 * DWG;  // [DWG][2]  group accumulator complete
+  uint64_t* dempty = dfull + 2 * DWG;  // [DWG][2]  epilogue drained it
+  unsigned long long* wprof = reinterpret_cast<unsigned long long*>(dempty + 2 * DWG);   // [8] wait cycles
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wprof + 8);
+  int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+  // wait accounting slots (OWQ_TRACE): 0 decode/full 1 decode/aempty 2 mma/afull
+  // 3 mma/dempty 4 epi/full 5 epi/dfull 6 prod/empty
+  unsigned long long* const WP = p.trace ? wprof : nullptr;
 
   const int64_t grid = gridDim.x, cta = blockIdx.x;
   // the host caps the grid so that every CTA's byte window holds an item start
   const int64_t i0 = cta_first_item(g, grid, cta), i1 = cta_first_item(g, grid, cta + 1);
-  if (p.trace && threadIdx.x == 0) p.trace[cta * 64 + 0] = gtime();
-  const int glog = p.group_log2;
+  if (p.trace && threadIdx.x == 0) p.trace[cta * 256 + 0] = gtime();
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NW); }
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); }
+    for (int i = 0; i < 2 * DWG; ++i) {
+      mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int i = 0; i < 8; ++i) wprof[i] = 0ull;
   }
+  if (warp == C::kProdWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                 "n"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // x tiles start zeroed: rows >= B of the UMMA B operand are never written
+  for (int i = threadIdx.x; i < DWG * 2 * C::kIPB * kXcBytes / 16; i += C::kThreads)
+    reinterpret_cast<uint4*>(xc)[i] = make_uint4(0, 0, 0, 0);
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_rb = items_per_rb(g);
 
-  if (warp == NW) {
-    // ------------------------------------------------------------------ producer
-    if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
+  if (p.dbg == 6 && warp != C::kProdWarp) {
+    if (warp < C::kEpiWarp0 + 4 || warp >= C::kMmaWarp0) {
       StageIter it;
-      it.init(g, i0, i1, CAP);
+      it.init(g, i0, i1, p.cap);
+      int64_t srb;
+      int32_t sli, n;
+      int s = 0;
+      uint32_t ph = 0;
+      const bool is_mma = warp >= C::kMmaWarp0;
+      while ((n = it.next(srb, sli)) > 0) {
+        if (!is_mma) {
+          mbar_wait(&full[s], ph);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        } else if (X1 && lane == 0) {
+          mbar_wait(&full[s], ph);
+          mbar_arrive(&empty[s]);
+        }
+        if (++s == NST) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else if (warp == C::kProdWarp) {
+    // ==================================================================== producer
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy(), pol_x = evict_last_policy();
+      StageIter it;
+      it.init(g, i0, i1, p.cap);
       int64_t srb;
       int32_t sli, n;
       int s = 0, k = 0;
       uint32_t ph = 0;
       while ((n = it.next(srb, sli)) > 0) {
-        if (k >= NST) mbar_wait(&empty[s], ph ^ 1u);
-        uint8_t* st = ring + (size_t)s * sg.bytes;
+        if (k >= NST) mbar_wait_p(&empty[s], ph ^ 1u, WP ? WP + 6 : nullptr);
+        if (p.dbg == 4 || p.dbg == 5) {   // experiments: plain bulk copies (no L2 hint) / codes only
+          uint8_t* st = ring + (size_t)s * p.stage_bytes;
+          const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
+          uint32_t tot = cbytes;
+          int64_t col0 = (int64_t)sli * kSuperStep;
+          int xcols = 0, gi0 = 0, ngrp = 0;
+          if (sli < g.nss && p.dbg == 4) {
+            const int ncols = n * kSuperStep;
+            xcols = (int)(p.xK - col0 < ncols ? p.xK - col0 : ncols);
+            gi0 = group_of(p, sli);
+            ngrp = group_of(p, sli + n - 1) - gi0 + 1;
+            tot += (uint32_t)(p.B * xcols * 2 + ngrp * kSZBlockBytes);
+          }
+          mbar_expect_tx(&full[s], tot);
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_addr(st)), "l"(p.blob + g.units_off + item_offset(g, srb, sli)), "r"(cbytes), "r"(smem_addr(&full[s])) : "memory");
+          if (xcols) {
+            for (int b = 0; b < p.B; ++b)
+              asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                               smem_addr(st + p.code_bytes + b * p.xraw_stride)), "l"(p.x + (int64_t)b * p.xK + col0), "r"(xcols * 2), "r"(smem_addr(&full[s])) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             smem_addr(st + p.sz_off)), "l"(p.blob + g.sz_off + (srb * g.G + gi0) * kSZBlockBytes), "r"(ngrp * kSZBlockBytes), "r"(smem_addr(&full[s])) : "memory");
+          }
+          ++k;
+          if (++s == NST) { s = 0; ph ^= 1u; }
+          continue;
+        }
+        if (p.trace && k < 32) p.trace[cta * 256 + 64 + k] = gtime();
+        uint8_t* st = ring + (size_t)s * p.stage_bytes;
         const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
         if (sli < g.nss) {
           const int64_t col0 = (int64_t)sli * kSuperStep;
@@ -254,15 +423,15 @@ __global__ void __launch_bounds__((NW + 1) * 32) __maxnreg__(NW >= 15 ? 128 : 22
           if (xcols < ncols)   // zero the columns past K (their codes meet x = 0)
             for (int b = 0; b < p.B; ++b)
               for (int c = xcols; c < ncols; ++c)
-                reinterpret_cast<__half*>(st + sg.code_bytes + b * sg.xstride)[c] = __float2half(0.f);
-          const int gi0 = g.group ? (int)(sli >> glog) : 0;
-          const int ngrp = g.group ? (int)((sli + n - 1) >> glog) - gi0 + 1 : 1;
+                reinterpret_cast<__half*>(st + p.code_bytes + b * p.xraw_stride)[c] = __float2half(0.f);
+          const int gi0 = group_of(p, sli);
+          const int ngrp = group_of(p, sli + n - 1) - gi0 + 1;
           mbar_expect_tx(&full[s], cbytes + (uint32_t)(p.B * xcols * 2 + ngrp * kSZBlockBytes));
           bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
           for (int b = 0; b < p.B; ++b)
-            bulk_g2s(st + sg.code_bytes + b * sg.xstride, p.x + (int64_t)b * p.xK + col0, (uint32_t)(xcols * 2),
-                     &full[s], 0ull);
-          bulk_g2s(st + sg.code_bytes + sg.x_bytes, p.blob + g.sz_off + (srb * g.G + gi0) * kSZBlockBytes,
+            bulk_g2s(st + p.code_bytes + b * p.xraw_stride, p.x + (int64_t)b * p.xK + col0, (uint32_t)(xcols * 2),
+                     &full[s], pol_x);
+          bulk_g2s(st + p.sz_off, p.blob + g.sz_off + (srb * g.G + gi0) * kSZBlockBytes,
                    (uint32_t)(ngrp * kSZBlockBytes), &full[s], pol);
         } else {
           mbar_expect_tx(&full[s], cbytes);
@@ -272,298 +441,362 @@ __global__ void __launch_bounds__((NW + 1) * 32) __maxnreg__(NW >= 15 ? 128 : 22
         if (++s == NST) { s = 0; ph ^= 1u; }
       }
     }
-    return;
-  }
-
-  // -------------------------------------------------------------------- consumers
-  const int tid = threadIdx.x;
-  {  // x gathered at the weak columns, x[b][idx[t]] (0 for padding); synced lazily
-    const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
-    for (int i = tid; i < p.B * g.kpad; i += NW * 32) {
-      const int b = i / g.kpad, t = i - b * g.kpad;
-      xw[i] = t < g.k ? p.x[(int64_t)b * p.xK + widx[t]] : __float2half(0.f);
-    }
-  }
-  bool xw_ready = false;
-  float* myred = red + warp * RED_PER_WARP + lane * 4 * NB;   // [r][lane][c], stride 32*4*NB per r
+  } else if (warp < C::kDecodeWarps) {
+    // ==================================================================== decode
+    const int wg = warp >> 2, q = warp & 3;
+    const int row = q * 32 + lane;                      // TMEM lane / row inside the row-block
+    const int wt = threadIdx.x & 127;                   // thread index inside the warpgroup
+    using D = Decoder<BITS>;
+    uint32_t magic;
+    asm volatile("mov.b32 %0, %1;" : "=r"(magic) : "n"(kFp16Magic));
+    uint32_t cz[D::NP];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+    for (int i = 0; i < D::NP; ++i) cz[i] = 0u;
+    int64_t key_rb = -1;
+    int key_gi = -1;
+    uint32_t acnt = 0;          // A-buffer uses
+    const uint32_t xc_wg = smem_addr(xc) + (uint32_t)(wg * 2 * C::kIPB * kXcBytes);
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int xb_ = wt >> 3, xkc = wt & 7;
+    const bool xthr = wt < p.B * 8;
+    StageIter it;
+    it.init(g, i0, i1, p.cap);
+    int64_t srb;
+    int32_t sli, n;
+    int s = 0;
+    uint32_t ph = 0;
+    int kst = 0;
+    while ((n = it.next(srb, sli)) > 0) {
+      mbar_wait_p(&full[s], ph, WP ? WP + 0 : nullptr);
+      if (p.trace && warp == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 192 + kst] = gtime();
+      const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
+      if (sli < g.nss) {
+        const int gi0 = group_of(p, sli);
+        int lo, hi;
+        share(n, wg, DWG, lo, hi);
+        for (int pa = lo; pa < hi; pa += C::kIPB) {
+          const uint32_t buf = acnt & 1u, aph = (acnt >> 1) & 1u;
+          if (acnt >= 2) mbar_wait_p(&aempty[wg * 2 + buf], aph ^ 1u, WP ? WP + 1 : nullptr);
+          ++acnt;
+          tc_fence_after();
+          const int pe = pa + C::kIPB < hi ? pa + C::kIPB : hi;
+          for (int pi = pa; pi < pe; ++pi) {
+            const int gi = group_of(p, sli + pi);
+            if (srb != key_rb || gi != key_gi) {
+              const uint32_t sz = lds32(sbase + p.sz_off + (gi - gi0) * kSZBlockBytes + row * 4);
+              const __half2 zz = __high2half2(u2h(sz));
 #pragma unroll
-    for (int c = 0; c < 4 * NB; c += 4)
-      *reinterpret_cast<float4*>(myred + r * 32 * 4 * NB + c) = make_float4(0.f, 0.f, 0.f, 0.f);
-
-  using D = Dec<BITS>;
-  constexpr int NP = D::NP;
-  float acc[4][4 * NB];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4 * NB; ++c) acc[r][c] = 0.f;
-  float sc[4][2];                  // scales of the lane's 8 rows, current group
-  uint32_t cz[4][2][NP];           // HFMA2 constants -(1024*2^-p + z)
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      sc[r][h] = 0.f;
-#pragma unroll
-      for (int q = 0; q < NP; ++q) cz[r][h][q] = 0u;
-    }
-  int64_t key_rb = -1;             // (row-block, group) whose scale acc[] still owes
-  int key_gi = -1;
-  bool acc_dirty = false;
-  uint32_t magic;                  // kFp16Magic, opaque so LOP3 keeps it in a register
-  asm volatile("mov.b32 %0, %1;" : "=r"(magic) : "n"(kFp16Magic));
-  const int bx0 = gq < p.B ? gq : p.B - 1;            // batch row of this lane (n-tile 0)
-  const int bx1 = 8 + gq < p.B ? 8 + gq : p.B - 1;    // n-tile 1
-  const uint32_t xoff0 = sg.code_bytes + bx0 * sg.xstride + tq * 32;
-  const uint32_t xoff1 = sg.code_bytes + bx1 * sg.xstride + tq * 32;
-  const uint32_t szoff = sg.code_bytes + sg.x_bytes + gq * 32;
-
-  // acc -> running sums in smem, times the scale owed (1 for weak products)
-  auto flush = [&](bool scaled) {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const float s0 = scaled ? sc[r][0] : 1.f;
-      const float s1 = scaled ? sc[r][1] : 1.f;
-#pragma unroll
-      for (int c = 0; c < 4 * NB; c += 4) {
-        float4* q = reinterpret_cast<float4*>(myred + r * 32 * 4 * NB + c);
-        float4 v = *q;
-        v.x = fmaf(s0, acc[r][c], v.x);
-        v.y = fmaf(s0, acc[r][c + 1], v.y);
-        v.z = fmaf(s1, acc[r][c + 2], v.z);
-        v.w = fmaf(s1, acc[r][c + 3], v.w);
-        *q = v;
-        acc[r][c] = acc[r][c + 1] = acc[r][c + 2] = acc[r][c + 3] = 0.f;
-      }
-    }
-    acc_dirty = false;
-  };
-
-  StageIter it;
-  it.init(g, i0, i1, CAP);
-  int64_t crb, nrb = 0;
-  int32_t cli, nli = 0;
-  int32_t cn = it.next(crb, cli);
-  int slot = 0;
-  uint32_t ph = 0;
-  while (cn > 0) {
-    const int32_t nn = it.next(nrb, nli);
-    const uint32_t sbase = smem_addr(ring + (size_t)slot * sg.bytes);
-    if (cli < g.nss) {
-      // ---------------------------------------------------------- code stage
-      const int gi0 = g.group ? (int)(cli >> glog) : 0;
-      mbar_wait(&full[slot], ph);
-#pragma unroll 1
-      for (int j = 0; j < IPW; ++j) {
-        const int pos = warp * IPW + j;
-        if (pos >= cn) break;
-        const int gi = g.group ? (int)((cli + pos) >> glog) : 0;
-        if (crb != key_rb || gi != key_gi) {
-          if (acc_dirty) flush(true);
-          const uint32_t szb = sbase + szoff + (gi - gi0) * kSZBlockBytes;
-          const uint4 s0 = lds128(szb), s1 = lds128(szb + 16);
-          const uint32_t e8[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const __half2 sz = u2h(e8[2 * r + h]);
-              sc[r][h] = __low2float(sz);
-              const __half2 zz = __high2half2(sz);
-#pragma unroll
-              for (int q = 0; q < NP; ++q) cz[r][h][q] = h2u(__hneg2(__hadd2(u2h(D::base(q)), zz)));
+              for (int i = 0; i < D::NP; ++i) cz[i] = h2u(__hneg2(__hadd2(u2h(D::base(i)), zz)));
+              key_rb = srb;
+              key_gi = gi;
             }
-          key_rb = crb;
-          key_gi = gi;
-        }
-        uint32_t xr[NB][8];
-        {
-          const uint32_t xb = sbase + pos * (kSuperStep * 2);
-          const uint4 a0 = lds128(xb + xoff0), a1 = lds128(xb + xoff0 + 16);
-          xr[0][0] = a0.x; xr[0][1] = a0.y; xr[0][2] = a0.z; xr[0][3] = a0.w;
-          xr[0][4] = a1.x; xr[0][5] = a1.y; xr[0][6] = a1.z; xr[0][7] = a1.w;
-          if (NB == 2) {
-            const uint4 b0 = lds128(xb + xoff1), b1 = lds128(xb + xoff1 + 16);
-            xr[NB - 1][0] = b0.x; xr[NB - 1][1] = b0.y; xr[NB - 1][2] = b0.z; xr[NB - 1][3] = b0.w;
-            xr[NB - 1][4] = b1.x; xr[NB - 1][5] = b1.y; xr[NB - 1][6] = b1.z; xr[NB - 1][7] = b1.w;
+            const uint32_t ssb = sbase + (uint32_t)(pi * g.ss_bytes);
+            uint32_t w[8];
+            {
+              const uint4 a = lds128(ssb + row * 16);
+              w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+              if (BITS == 3) {
+                const uint2 b = lds64(ssb + 2048 + row * 8);
+                w[4] = b.x; w[5] = b.y;
+              } else {
+                const uint4 b = lds128(ssb + 2048 + row * 16);
+                w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+              }
+            }
+            uint4 xpiece = make_uint4(0, 0, 0, 0);
+            if (!X1 && xthr) xpiece = lds128(sbase + p.code_bytes + xb_ * p.xraw_stride + (pi * kSuperStep + xkc * 8) * 2);
+            uint32_t e[32];
+            if (p.dbg == 1) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) e[j] = w[j & 7];
+            } else {
+              D::run(w, magic, cz, e);
+            }
+            const int slot_i = pi - pa;   // item slot inside the A buffer
+            if (p.dbg != 2) tc_st32(trow + (uint32_t)((wg * 2 + buf) * C::kACols + slot_i * 32), e);
+            else if ((e[0] ^ e[7] ^ e[13] ^ e[31]) == 0x12345678u) asm volatile("trap;");
+            if (!X1 && xthr)
+              sts128(xc_wg + (uint32_t)((buf * C::kIPB + slot_i) * kXcBytes + (xkc * 2 + (xb_ >> 3)) * 128 + (xb_ & 7) * 16),
+                     xpiece);
           }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          if (!X1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // x tiles -> async proxy (MMA)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&afull[wg * 2 + buf]);
         }
-        const uint32_t ssb = sbase + (uint32_t)(pos * g.ss_bytes) + lane * 16;
-        constexpr int WPP = BITS == 3 ? 3 : 4;
-        uint32_t wv[4 * WPP];
-#pragma unroll
-        for (int l = 0; l < WPP; ++l) {
-          const uint4 q = lds128(ssb + l * 512);
-          wv[4 * l] = q.x; wv[4 * l + 1] = q.y; wv[4 * l + 2] = q.z; wv[4 * l + 3] = q.w;
-        }
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          uint32_t e[16];
-          if (BITS == 3) decode3(wv[3 * s], wv[3 * s + 1], wv[3 * s + 2], magic, e);
-          else decode4(&wv[4 * s], magic, e);
-#pragma unroll
-          for (int P = 0; P < 16; ++P) {
-            const int q = D::pidx(P);
-            e[P] = hfma2u(e[P], D::mul(q), cz[P >> 2][P & 1][q]);   // exact q - z
-          }
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            mma16816(&acc[r][0], &e[4 * r], xr[0][2 * s], xr[0][2 * s + 1]);
-            if (NB == 2) mma16816(&acc[r][4], &e[4 * r], xr[NB - 1][2 * s], xr[NB - 1][2 * s + 1]);
-          }
-        }
-        acc_dirty = true;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    } else {
-      // ---------------------------------------------------------- weak stage (unscaled)
-      if (!xw_ready) { named_sync_n(NW * 32); xw_ready = true; }
-      if (acc_dirty) flush(key_rb >= 0);
-      key_rb = -1;
-      key_gi = -1;
-      mbar_wait(&full[slot], ph);
-#pragma unroll 1
-      for (int j = 0; j < IPW; ++j) {
-        const int pos = warp * IPW + j;
-        if (pos >= cn) break;
-        const int gch = cli - g.nss + pos;                  // chunk index within the row-block
-        uint32_t av[8];
-        if (gch < g.nfull) {
-          const uint32_t cb = sbase + pos * kWeakChunkBytes + lane * 32;
-          const uint4 a01 = lds128(cb), a23 = lds128(cb + 16);
-          av[0] = a01.x; av[1] = a01.y; av[2] = a01.z; av[3] = a01.w;
-          av[4] = a23.x; av[5] = a23.y; av[6] = a23.z; av[7] = a23.w;
-        } else {   // ragged tail chunk, row-major [64][ktail]
-          const unsigned short* tl = reinterpret_cast<const unsigned short*>(
-              ring + (size_t)slot * sg.bytes + (size_t)pos * kWeakChunkBytes);
-          const int c0 = 2 * tq, kt = g.ktail;
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (p.trace && warp == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 96 + kst] = gtime();
+      ++kst;
+      if (++s == NST) { s = 0; ph ^= 1u; }
+    }
+  } else if (warp >= C::kMmaWarp0) {
+    // ==================================================================== MMA issue (one warp per warpgroup)
+    const int wg = warp - C::kMmaWarp0;
+    if (lane == 0) {
+      uint32_t acnt = 0, dcnt = 0;
+      bool open = false;          // D[dcnt & 1] holds a partial group sum
+      const uint32_t xc_wg = smem_addr(xc) + (uint32_t)(wg * 2 * C::kIPB * kXcBytes);
+      StageIter it;
+      it.init(g, i0, i1, p.cap);
+      int64_t crb, nrb = -1;
+      int32_t cli, nli = 0;
+      int32_t cn = it.next(crb, cli);
+      int s = 0, kst = 0;
+      while (cn > 0) {
+        const int32_t nn = it.next(nrb, nli);
+        if (cli < g.nss) {
+          const uint32_t sx = smem_addr(ring + (size_t)s * p.stage_bytes) + p.code_bytes;   // raw x (X1)
+          int lo, hi;
+          share(cn, wg, DWG, lo, hi);
+          uint32_t buf = 0;
+          for (int pa = 0; pa < cn;) {
+            const Seg sg = segment(p, pa, cn, cli, crb, nn, nrb, nli);
+            const int a0 = sg.pa > lo ? sg.pa : lo, a1 = sg.pb + 1 < hi ? sg.pb + 1 : hi;
+            for (int pi = a0; pi < a1; ++pi) {
+              const int slot_i = (pi - lo) % C::kIPB;
+              if (slot_i == 0) {   // first item of an A buffer: wait for its publish
+                buf = acnt & 1u;
+                const uint32_t aph = (acnt >> 1) & 1u;
+                ++acnt;
+                mbar_wait_p(&afull[wg * 2 + buf], aph, WP ? WP + 2 : nullptr);
+                tc_fence_after();
+              }
+              const uint32_t dbuf = dcnt & 1u;
+              if (!open && dcnt >= 2) mbar_wait_p(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u, WP ? WP + 3 : nullptr);
+              const uint32_t a_t = tmem + (uint32_t)((wg * 2 + buf) * C::kACols + slot_i * 32);
+              const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * kMmaN);
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int row = 16 * r + gq + 8 * h;
-              const uint32_t lo = c0 < kt ? tl[row * kt + c0] : 0u;
-              const uint32_t hi = c0 + 1 < kt ? tl[row * kt + c0 + 1] : 0u;
-              av[2 * r + h] = lo | (hi << 16);
+              for (int j = 0; j < 4; ++j) {
+                if (p.dbg == 3) break;
+                // X1: core matrix row 0 = x[16j + 8c ..], rows 1..7 read the following
+                // chunks (finite, they only feed D columns 1..15 which are ignored)
+                const uint64_t bd = X1 ? umma_desc(sx + (uint32_t)(pi * kSuperStep * 2 + j * 32), 16, 0)
+                                       : umma_desc(xc_wg + (buf * C::kIPB + slot_i) * kXcBytes + j * 512, 256, 128);
+                tc_mma_f16(d_t, a_t + 8 * j, bd, kIdesc, (open || j > 0) ? 1u : 0u);
+              }
+              open = true;
+              if (slot_i == C::kIPB - 1 || pi + 1 == hi) tc_commit(&aempty[wg * 2 + buf]);   // buffer consumed
             }
-        }
-        const int kc = gch * kWeakChunk + 2 * tq;
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xw + bx0 * g.kpad + kc);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          mma1688(&acc[r][0], av[2 * r], av[2 * r + 1], b0);
-          if (NB == 2) {
-            const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xw + bx1 * g.kpad + kc);
-            mma1688(&acc[r][4], av[2 * r], av[2 * r + 1], b1);
+            if (sg.ends && open) {
+              tc_commit(&dfull[wg * 2 + (dcnt & 1u)]);
+              ++dcnt;
+              open = false;
+            }
+            pa = sg.pb + 1;
           }
         }
-        acc_dirty = true;
+        if (X1) tc_commit(&empty[s]);   // the stage's x is free once these MMAs completed
+        if (p.trace && wg == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
+        ++kst;
+        if (++s == NST) s = 0;
+        crb = nrb;
+        cli = nli;
+        cn = nn;
+      }
+    }
+  } else {
+    // ==================================================================== epilogue
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int et = threadIdx.x - C::kEpiWarp0 * 32;     // 0..127
+    {  // x gathered at the weak columns, x[b][idx[t]] (0 for padding)
+      const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
+      for (int i = et; i < p.B * g.kpad; i += 128) {
+        const int b = i / g.kpad, t = i - b * g.kpad;
+        xw[i] = t < g.k ? p.x[(int64_t)b * p.xK + widx[t]] : __float2half(0.f);
+      }
+    }
+    named_sync(2, 128);
+    float tot[kMmaN];
+#pragma unroll
+    for (int b = 0; b < kMmaN; ++b) tot[b] = 0.f;
+    uint32_t dcnt[DWG];
+#pragma unroll
+    for (int w = 0; w < DWG; ++w) dcnt[w] = 0;
+    uint32_t part = 0;                                   // warpgroups with items in the open group
+    int kst = 0;
+    StageIter it;
+    it.init(g, i0, i1, p.cap);
+    int64_t crb, nrb = -1;
+    int32_t cli, nli = 0;
+    int32_t cn = it.next(crb, cli);
+    int s = 0;
+    uint32_t ph = 0;
+    while (cn > 0) {
+      const int32_t nn = it.next(nrb, nli);
+      mbar_wait_p(&full[s], ph, WP ? WP + 4 : nullptr);
+      const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
+      if (cli < g.nss) {
+        const int gi0 = group_of(p, cli);
+        for (int pa = 0; pa < cn;) {
+          const Seg sg = segment(p, pa, cn, cli, crb, nn, nrb, nli);
+#pragma unroll
+          for (int w = 0; w < DWG; ++w) {
+            int lo, hi;
+            share(cn, w, DWG, lo, hi);
+            if (lo <= sg.pb && hi > sg.pa) part |= 1u << w;
+          }
+          if (sg.ends) {
+            const float s_g = __low2float(u2h(lds32(sbase + p.sz_off + (sg.gi - gi0) * kSZBlockBytes + row * 4)));
+            float sum[kMmaN];
+#pragma unroll
+            for (int b = 0; b < kMmaN; ++b) sum[b] = 0.f;
+#pragma unroll
+            for (int w = 0; w < DWG; ++w) {
+              if (part & (1u << w)) {   // fixed order over warpgroups: deterministic
+                const uint32_t dbuf = dcnt[w] & 1u;
+                mbar_wait_p(&dfull[w * 2 + dbuf], (dcnt[w] >> 1) & 1u, WP ? WP + 5 : nullptr);
+                tc_fence_after();
+                uint32_t d[kMmaN];
+                tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * kMmaN), d);
+#pragma unroll
+                for (int b = 0; b < kMmaN; ++b) sum[b] += __uint_as_float(d[b]);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&dempty[w * 2 + dbuf]);
+                ++dcnt[w];
+              }
+            }
+#pragma unroll
+            for (int b = 0; b < kMmaN; ++b) tot[b] = fmaf(s_g, sum[b], tot[b]);
+            part = 0;
+          }
+          pa = sg.pb + 1;
+        }
+      } else {
+        // weak chunks: fp16 weak columns x gathered activations, fp32 (unscaled)
+        for (int pi = 0; pi < cn; ++pi) {
+          const int gch = cli - g.nss + pi;
+          float v[8];
+          if (gch < g.nfull) {
+            const uint4 a = lds128(sbase + pi * kWeakChunkBytes + row * 16);
+            const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float2 f = __half22float2(u2h(aw[c]));
+              v[2 * c] = f.x;
+              v[2 * c + 1] = f.y;
+            }
+          } else {
+            const __half* tl = reinterpret_cast<const __half*>(ring + (size_t)s * p.stage_bytes + (size_t)pi * kWeakChunkBytes);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = c < g.ktail ? __half2float(tl[row * g.ktail + c]) : 0.f;
+          }
+#pragma unroll
+          for (int b = 0; b < kMmaN; ++b) {
+            if (b < p.B) {
+              const uint4 xv = *reinterpret_cast<const uint4*>(xw + b * g.kpad + gch * kWeakChunk);
+              const uint32_t xwv[4] = {xv.x, xv.y, xv.z, xv.w};
+              float acc = tot[b];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const float2 f = __half22float2(u2h(xwv[c]));
+                acc = fmaf(v[2 * c], f.x, acc);
+                acc = fmaf(v[2 * c + 1], f.y, acc);
+              }
+              tot[b] = acc;
+            }
+          }
+        }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-    if (++slot == NST) { slot = 0; ph ^= 1u; }
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (p.trace && et == 0 && kst < 32) p.trace[cta * 256 + 160 + kst] = gtime();
+      ++kst;
+      if (++s == NST) { s = 0; ph ^= 1u; }
 
-    if (nn == 0 || nrb != crb) {
-      // ------------------------------------------------------ finish row-block crb
-      if (p.trace && tid == 0) p.trace[cta * 64 + 50] = gtime();
-      if (!xw_ready) { named_sync_n(NW * 32); xw_ready = true; }
-      if (acc_dirty) flush(key_rb >= 0);
-      key_rb = -1;
-      key_gi = -1;
-      named_sync_n(NW * 32);
-      const int n_rb = items_per_rb(g);
-      const int64_t ifirst = crb * n_rb, ilast = ifirst + n_rb - 1;
-      const bool whole = ifirst >= i0 && ilast < i1;
-      const int nout = kRowBlock * p.B;
-      for (int o = tid; o < nout; o += NW * 32) {
-        const int b = o / kRowBlock, il = o - b * kRowBlock;
-        const int r = il >> 4, rem = il & 15, rg = rem & 7, h = rem >> 3;
-        const int nt = b >> 3, bb = b & 7;
-        const int src = (r * 32 + rg * 4 + (bb >> 1)) * 4 * NB + nt * 4 + h * 2 + (bb & 1);
-        float v = 0.f;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) v += red[w * RED_PER_WARP + src];
-        const int64_t row = crb * kRowBlock + il;
+      if (nn == 0 || nrb != crb) {
+        // -------------------------------------------------- finish row-block crb
+        if (p.trace && et == 0) p.trace[cta * 256 + 50] = gtime();
+        const int64_t ifirst = crb * n_rb, ilast = ifirst + n_rb - 1;
+        const bool whole = ifirst >= i0 && ilast < i1;
+        const int64_t grow = crb * kRowBlock + row;
         if (whole) {
-          if (row < g.M) {
-            if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + row] = v;
-            else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + row] = __float2half_rn(v);
+          if (grow < g.M) {
+#pragma unroll
+            for (int b = 0; b < kMmaN; ++b)
+              if (b < p.B) {
+                if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = tot[b];
+                else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(tot[b]);
+              }
           }
         } else {
-          __stcg(&p.partial[((crb + cta) * p.B + b) * kRowBlock + il], v);
-        }
-      }
-      if (!whole) {
-        // pieces = CTAs cta_of(first item) .. cta_of(last item) (none is empty)
-        const int64_t c_first = cta_of_item(g, grid, ifirst), c_last = cta_of_item(g, grid, ilast);
-        const int npieces = (int)(c_last - c_first + 1);
-        named_sync_n(NW * 32);
-        if (tid == 0) {
-          // acq_rel: releases this CTA's partial stores (ordered before by the
-          // barrier), acquires the other pieces' stores when we are last
-          unsigned old;
-          asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counters + crb) : "memory");
-          const int last = old == (unsigned)(npieces - 1);
-          if (last) p.counters[crb] = 0u;   // all pieces arrived: reset for the next call
-          *flag = last;
-        }
-        named_sync_n(NW * 32);
-        if (*flag) {
-          for (int o = tid; o < nout; o += NW * 32) {
-            const int b = o / kRowBlock, il = o - b * kRowBlock;
-            float v = 0.f;
-            for (int q = 0; q < npieces; ++q)
-              v += __ldcg(&p.partial[((crb + c_first + q) * p.B + b) * kRowBlock + il]);
-            const int64_t row = crb * kRowBlock + il;
-            if (row < g.M) {
-              if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + row] = v;
-              else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + row] = __float2half_rn(v);
+#pragma unroll
+          for (int b = 0; b < kMmaN; ++b)
+            if (b < p.B) __stcg(&p.partial[((crb + cta) * p.B + b) * kRowBlock + row], tot[b]);
+          // pieces = CTAs cta_of(first item) .. cta_of(last item) (none is empty)
+          const int64_t c_first = cta_of_item(g, grid, ifirst), c_last = cta_of_item(g, grid, ilast);
+          const int npieces = (int)(c_last - c_first + 1);
+          named_sync(2, 128);
+          if (et == 0) {
+            // acq_rel: releases this CTA's partial stores (ordered before by the
+            // barrier), acquires the other pieces' stores when we are last
+            unsigned old;
+            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counters + crb) : "memory");
+            const int last = old == (unsigned)(npieces - 1);
+            if (last) p.counters[crb] = 0u;   // all pieces arrived: reset for the next call
+            *flag = last;
+          }
+          named_sync(2, 128);
+          if (*flag && grow < g.M) {
+            for (int b = 0; b < p.B; ++b) {
+              float v = 0.f;
+              for (int qq = 0; qq < npieces; ++qq)
+                v += __ldcg(&p.partial[((crb + c_first + qq) * p.B + b) * kRowBlock + row]);
+              if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = v;
+              else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(v);
             }
           }
+          named_sync(2, 128);
         }
+#pragma unroll
+        for (int b = 0; b < kMmaN; ++b) tot[b] = 0.f;
+        if (p.trace && et == 0) p.trace[cta * 256 + 56] = gtime();
       }
-      named_sync_n(NW * 32);
-      if (p.trace && tid == 0) p.trace[cta * 64 + 56] = gtime();
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4 * NB; c += 4)
-          *reinterpret_cast<float4*>(myred + r * 32 * 4 * NB + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      crb = nrb;
+      cli = nli;
+      cn = nn;
     }
-    crb = nrb;
-    cli = nli;
-    cn = nn;
   }
-  if (p.trace && tid == 0) p.trace[cta * 64 + 62] = gtime();
+  // teardown: every role is done with TMEM
+  tc_fence_before();
+  __syncthreads();
+  if (warp == C::kProdWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
+  }
+  if (p.trace && threadIdx.x == 0) {
+    p.trace[cta * 256 + 62] = gtime();
+    for (int i = 0; i < 8; ++i) p.trace[cta * 256 + 10 + i] = wprof[i];
+  }
 }
 
-// Device inverse of the code layout (test hook): one warp per (row-block, super-step).
+// Device inverse of the code layout (test hook): one CTA (128 threads = rows) per
+// (row-block, super-step).
 __global__ void owq_unpack_codes_kernel(const uint8_t* blob, Geo g, uint8_t* codes) {
   const int64_t item = blockIdx.x;
   const int rb = (int)(item / g.nss), ss = (int)(item % g.nss);
-  const int lane = threadIdx.x, gq = lane >> 2, t = lane & 3;
+  const int rr = threadIdx.x;
+  const int64_t row = (int64_t)rb * kRowBlock + rr;
+  if (row >= g.M) return;
   const uint8_t* rec = blob + g.units_off + (int64_t)rb * g.rb_bytes + (int64_t)ss * g.ss_bytes;
-  const int wpp = words_per_packet(g.bits);
-  for (int s = 0; s < 4; ++s) {
-    uint32_t w[4];
-    for (int i = 0; i < wpp; ++i) w[i] = *reinterpret_cast<const uint32_t*>(rec + lane_word_byte(s * wpp + i, lane));
-    for (int P = 0; P < 16; ++P)
-      for (int half = 0; half < 2; ++half) {
-        const int row = rb * kRowBlock + pair_row(P, gq), col = ss * kSuperStep + pair_col(P, t, s, half);
-        if (row >= g.M || col >= g.K) continue;
-        uint32_t c = 0;
-        for (int bit = 0; bit < g.bits; ++bit) {
-          int word, pos;
-          code_bit_loc(g.bits, P, half, bit, word, pos);
-          c |= ((w[word] >> pos) & 1u) << bit;
-        }
-        codes[(int64_t)row * g.K + col] = (uint8_t)c;
+  uint32_t w[8];
+  for (int i = 0; i < words_per_row(g.bits); ++i) w[i] = *reinterpret_cast<const uint32_t*>(rec + row_word_byte(g.bits, rr, i));
+  for (int j = 0; j < kSuperStep / 2; ++j)
+    for (int half = 0; half < 2; ++half) {
+      const int64_t col = (int64_t)ss * kSuperStep + 2 * j + half;
+      if (col >= g.K) continue;
+      uint32_t c = 0;
+      for (int bit = 0; bit < g.bits; ++bit) {
+        int word, pos;
+        code_bit_loc(g.bits, j, half, bit, word, pos);
+        c |= ((w[word] >> pos) & 1u) << bit;
       }
-  }
+      codes[row * g.K + col] = (uint8_t)c;
+    }
 }
 
 // ---------------------------------------------------------------- host side
@@ -598,8 +831,8 @@ static owq_status check_blob(const owq_shape* s, const void* d_packed, Geo& g) {
   return OWQ_OK;
 }
 
-// Header checks cost a device->host copy; cache the last verified blob pointer
-// per shape so the hot path does not synchronise (the blob is immutable).
+// Header checks cost a device->host copy; cache verified blob pointers per shape
+// so the hot path does not synchronise (the blob is immutable).
 struct BlobCacheEntry { const void* ptr; owq_shape s; };
 static thread_local BlobCacheEntry g_blob_cache[16];
 static thread_local int g_blob_cache_next = 0;
@@ -618,7 +851,7 @@ static owq_status check_blob_cached(const owq_shape* s, const void* d_packed, Ge
   return st;
 }
 
-// Workspace: [counters nrb u32][partials (nrb + grid) x B x 64 f32][x pad B x Kp f16]
+// Workspace: [counters nrb u32][partials (nrb + grid) x B x 128 f32][x pad B x Kp f16]
 static size_t ws_counters(const Geo& g) { return ((size_t)g.nrb * 4 + 255) / 256 * 256; }
 static size_t ws_partials(const Geo& g, int B, int64_t G) {
   return ((size_t)(g.nrb + G) * B * kRowBlock * 4 + 255) / 256 * 256;
@@ -627,50 +860,46 @@ static size_t ws_bytes_for(const Geo& g, int B, int64_t G) {
   return ws_counters(g) + ws_partials(g, B, G) + (size_t)B * g.nss * kSuperStep * 2;
 }
 
-// Kernel configurations: NW consumer warps, IPW items (super-steps) per warp per
-// stage.
-template <int BITS, int NB, int NW, int IPW>
+template <int BITS, int DWG, bool X1>
 static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
+  using C = Cfg<BITS, DWG, X1>;
   Params p = p0;
-  const int64_t cap = (int64_t)NW * IPW;
-  p.sg.code_bytes = (int32_t)std::max<int64_t>(cap * p.g.ss_bytes, cap * kWeakChunkBytes);
-  p.sg.xstride = (int32_t)(cap * kSuperStep * 2 + 16);
-  p.sg.x_bytes = p.B * p.sg.xstride;
-  p.sg.sz_blocks = p.g.group ? (int32_t)(cap * kSuperStep / p.g.group + 2) : 1;
-  p.sg.bytes = (p.sg.code_bytes + p.sg.x_bytes + p.sg.sz_blocks * kSZBlockBytes + 127) / 128 * 128;
-  const size_t red = (size_t)NW * 4 * 32 * 4 * NB * 4;
-  const size_t xw = (((size_t)p.B * p.g.kpad + 7) & ~(size_t)7) * 2;
+  p.cap = DWG * (BITS == 3 ? 4 : 2);
+  p.code_bytes = (int32_t)std::max<int64_t>((int64_t)p.cap * p.g.ss_bytes, (int64_t)p.cap * kWeakChunkBytes);
+  p.xraw_stride = p.cap * kSuperStep * 2;
+  p.sz_off = p.code_bytes + p.B * p.xraw_stride;
+  const int sz_blocks = p.g.group ? (int)(p.cap * kSuperStep / p.g.group + 2) : 1;
+  p.stage_bytes = (p.sz_off + sz_blocks * kSZBlockBytes + 127) / 128 * 128;
+  const size_t fixed = (size_t)DWG * 2 * C::kIPB * kXcBytes + (((size_t)p.B * p.g.kpad + 7) & ~(size_t)7) * 2 + 512;
   int dev = 0, maxsmem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t fixed = red + xw + 16;
-  int64_t avail = (int64_t)maxsmem - (int64_t)fixed - 64;
-  int nst = (int)(avail / (p.sg.bytes + 16));
+  const int64_t avail = (int64_t)maxsmem - (int64_t)fixed - 1024;
+  int nst = (int)(avail / (p.stage_bytes + 16));
   static const int max_nst = getenv("OWQ_NST") ? atoi(getenv("OWQ_NST")) : 8;
-  nst = nst > max_nst ? max_nst : nst;
+  nst = std::min(nst, max_nst);
   if (nst < 2) return OWQ_ERR_UNSUPPORTED;     // too many weak columns / batch rows for shared memory
   p.nst = nst;
-  const size_t smem = (size_t)nst * p.sg.bytes + fixed + (size_t)nst * 16 + 16;
-  auto kern = owq_gemv_kernel<BITS, NB, NW, IPW>;
+  const size_t smem = (size_t)nst * p.stage_bytes + fixed + (size_t)nst * 16;
+  auto kern = owq_gemv_kernel<BITS, DWG, X1>;
   static thread_local size_t configured = 0;
   if (configured < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return OWQ_ERR_CUDA;
     configured = smem;
   }
-  kern<<<(unsigned)grid, (NW + 1) * 32, smem, stream>>>(p);
+  kern<<<(unsigned)grid, C::kThreads, smem, stream>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    fprintf(stderr, "owq: launch of owq_gemv_kernel<%d,%d,%d,%d> (grid %lld, smem %zu) failed: %s\n", BITS, NB,
-            NW, IPW, (long long)grid, smem, cudaGetErrorString(e));
+    fprintf(stderr, "owq: launch of owq_gemv_kernel<%d,%d,%d> (grid %lld, smem %zu) failed: %s\n", BITS, DWG, (int)X1,
+            (long long)grid, smem, cudaGetErrorString(e));
     return OWQ_ERR_CUDA;
   }
   return OWQ_OK;
 }
 
-static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int B,
-                            void* d_y, int y_f32, void* d_ws, size_t ws_bytes, int grid_req,
-                            void* stream) {
+static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int B, void* d_y,
+                            int y_f32, void* d_ws, size_t ws_bytes, int grid_req, void* stream) {
   if (!d_x || !d_y || !d_ws) return OWQ_ERR_INVALID_ARG;
   if (B < 1 || B > OWQ_MAX_BATCH) return OWQ_ERR_UNSUPPORTED;
   Geo g;
@@ -701,23 +930,25 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   }
   static unsigned long long* trace_buf = nullptr;
   static const char* trace_path = getenv("OWQ_TRACE");
-  if (trace_path && !trace_buf) cudaMalloc(&trace_buf, 4096 * 64 * 8);
-  if (trace_buf) cudaMemsetAsync(trace_buf, 0, 4096 * 64 * 8, cs);
+  if (trace_path && !trace_buf) cudaMalloc(&trace_buf, 4096 * 256 * 8);
+  if (trace_buf) cudaMemsetAsync(trace_buf, 0, 4096 * 256 * 8, cs);
   p.trace = trace_buf;
+  static const int dbg = getenv("OWQ_DEBUG") ? atoi(getenv("OWQ_DEBUG")) : 0;
+  p.dbg = dbg;
   p.group_log2 = 0;
   if (g.group) while ((kSuperStep << p.group_log2) < g.group) ++p.group_log2;
-  const bool nb2 = B > 8;
+  static const int dwg = getenv("OWQ_DWG") ? atoi(getenv("OWQ_DWG")) : 3;
   owq_status rs;
-  static const int cfg = getenv("OWQ_CFG") ? atoi(getenv("OWQ_CFG")) : 0;
-  if (cfg == 1) {   // experiment: 8 consumer warps x 2 items
-    if (g.bits == 3) rs = nb2 ? launch<3, 2, 8, 2>(p, grid, cs) : launch<3, 1, 8, 2>(p, grid, cs);
-    else rs = nb2 ? launch<4, 2, 8, 2>(p, grid, cs) : launch<4, 1, 8, 2>(p, grid, cs);
+  const bool x1 = B == 1;
+  if (dwg == 2) {
+    if (g.bits == 3) rs = x1 ? launch<3, 2, true>(p, grid, cs) : launch<3, 2, false>(p, grid, cs);
+    else rs = x1 ? launch<4, 2, true>(p, grid, cs) : launch<4, 2, false>(p, grid, cs);
   } else {
-    if (g.bits == 3) rs = nb2 ? launch<3, 2, 8, 2>(p, grid, cs) : launch<3, 1, 15, 1>(p, grid, cs);
-    else rs = nb2 ? launch<4, 2, 8, 2>(p, grid, cs) : launch<4, 1, 15, 1>(p, grid, cs);
+    if (g.bits == 3) rs = x1 ? launch<3, 3, true>(p, grid, cs) : launch<3, 3, false>(p, grid, cs);
+    else rs = x1 ? launch<4, 3, true>(p, grid, cs) : launch<4, 3, false>(p, grid, cs);
   }
   if (trace_buf && rs == OWQ_OK) {   // experiments only: dump the per-CTA stamps
-    std::vector<unsigned long long> h((size_t)grid * 64);
+    std::vector<unsigned long long> h((size_t)grid * 256);
     cudaMemcpyAsync(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost, cs);
     cudaStreamSynchronize(cs);
     if (FILE* f = fopen(trace_path, "ab")) { fwrite(h.data(), 8, h.size(), f); fclose(f); }
@@ -731,8 +962,8 @@ using namespace owq;
 
 extern "C" {
 
-owq_status owq_pack(const owq_shape* s, const owq_host_layer* L, int flags, void* d_packed,
-                    size_t d_bytes, void* stream) {
+owq_status owq_pack(const owq_shape* s, const owq_host_layer* L, int flags, void* d_packed, size_t d_bytes,
+                    void* stream) {
   if (!d_packed) return OWQ_ERR_INVALID_ARG;
   const size_t n = owq_packed_bytes(s);
   if (n == 0) return OWQ_ERR_UNSUPPORTED;
@@ -751,7 +982,7 @@ owq_status owq_unpack_codes(const owq_shape* s, const void* d_packed, uint8_t* d
   Geo g;
   owq_status st = check_blob(s, d_packed, g);
   if (st != OWQ_OK) return st;
-  owq_unpack_codes_kernel<<<(unsigned)((int64_t)g.nrb * g.nss), 32, 0, (cudaStream_t)stream>>>(
+  owq_unpack_codes_kernel<<<(unsigned)((int64_t)g.nrb * g.nss), kRowBlock, 0, (cudaStream_t)stream>>>(
       (const uint8_t*)d_packed, g, d_codes);
   return cudaGetLastError() == cudaSuccess ? OWQ_OK : OWQ_ERR_CUDA;
 }
@@ -762,19 +993,18 @@ size_t owq_workspace_bytes(const owq_shape* s, int batch) {
   return ws_bytes_for(g, batch, device_sms());   // any k and the default grid fit
 }
 
-owq_status owq_gemv(const owq_shape* s, const void* d_packed, const uint16_t* d_x, void* d_y, int y_f32,
-                    void* d_ws, size_t ws_bytes, void* stream) {
+owq_status owq_gemv(const owq_shape* s, const void* d_packed, const uint16_t* d_x, void* d_y, int y_f32, void* d_ws,
+                    size_t ws_bytes, void* stream) {
   return gemm_impl(s, d_packed, d_x, 1, d_y, y_f32, d_ws, ws_bytes, 0, stream);
 }
 
-owq_status owq_gemm_small_batch(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int batch,
-                                void* d_y, int y_f32, void* d_ws, size_t ws_bytes, void* stream) {
+owq_status owq_gemm_small_batch(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int batch, void* d_y,
+                                int y_f32, void* d_ws, size_t ws_bytes, void* stream) {
   return gemm_impl(s, d_packed, d_x, batch, d_y, y_f32, d_ws, ws_bytes, 0, stream);
 }
 
-owq_status owq_gemm_small_batch_grid(const owq_shape* s, const void* d_packed, const uint16_t* d_x,
-                                     int batch, void* d_y, int y_f32, void* d_ws, size_t ws_bytes, int grid,
-                                     void* stream) {
+owq_status owq_gemm_small_batch_grid(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int batch,
+                                     void* d_y, int y_f32, void* d_ws, size_t ws_bytes, int grid, void* stream) {
   if (grid < 0) return OWQ_ERR_INVALID_ARG;
   return gemm_impl(s, d_packed, d_x, batch, d_y, y_f32, d_ws, ws_bytes, grid, stream);
 }

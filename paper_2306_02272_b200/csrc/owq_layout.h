@@ -1,6 +1,18 @@
-// owq_layout.h -- device layout of the packed OWQ blob (layout version 1).
+// owq_layout.h -- device layout of the packed OWQ blob (layout version 2).
 // Shared by the host packer (owq_pack.cpp) and the device kernels (*.cu).
-// The bit map is documented in DESIGN.md §5; include/owq.h summarises it.
+// DESIGN.md §5 documents the bit map; include/owq.h summarises it.
+//
+// Row-blocks of 128 output rows (one tcgen05 M=128 tile, one thread per row).
+// Per row-block: its super-steps (64 columns each) then its weak chunks.
+//   super-step record: every row's 64 codes in WPR 32-bit words (WPR = 6 for
+//     3-bit, 8 for 4-bit); words 0..3 of row r at r*16, words 4.. at
+//     2048 + r*(WPR-4)*4 -- one LDS.128 (+ one LDS.64/128) per thread, no bank
+//     conflicts.  Pair j = columns (2j, 2j+1) of the super-step becomes TMEM
+//     column j of the thread's row (fp16x2: low half = column 2j).
+//   weak chunk (8 weak columns): [128 rows][8] fp16; the ragged last chunk
+//     (k % 8 columns) is [128][k % 8] fp16, unpadded.
+// Then: scale/zero blocks [nrb][G][128 rows] of (s, z) fp16 pairs, and the
+// u16 weak-column index list.
 #pragma once
 #include <stdint.h>
 
@@ -12,27 +24,28 @@
 
 namespace owq {
 
-constexpr int kRowBlock = 64;        // rows per row-block (4 mma row-tiles of 16)
-constexpr int kSuperStep = 64;       // columns per super-step (4 mma k16 steps)
-constexpr int kWeakChunk = 8;        // weak columns per mma m16n8k8 chunk
-constexpr int kWeakChunkBytes = kRowBlock * kWeakChunk * 2;   // 1 KiB
+constexpr int kRowBlock = 128;       // rows per row-block (tcgen05 M = 128)
+constexpr int kSuperStep = 64;       // columns per super-step (4 MMAs of K = 16)
+constexpr int kWeakChunk = 8;        // weak columns per chunk
+constexpr int kWeakChunkBytes = kRowBlock * kWeakChunk * 2;   // 2 KiB
 constexpr int kHeaderBytes = 256;
-constexpr int kSZBlockBytes = kRowBlock * 4;                  // 64 x (s, z) fp16 pairs
+constexpr int kSZBlockBytes = kRowBlock * 4;                  // 128 x (s, z) fp16 pairs
 constexpr uint32_t kMagic = 0x4257514Fu;                      // "OQWB"
 
 OWQ_HD int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+OWQ_HD int words_per_row(int bits) { return bits == 3 ? 6 : 8; }
 
 struct Geo {
   int32_t M, K, bits, group, k;
   int32_t nrb;       // row-blocks
   int32_t nss;       // super-steps per row
   int32_t kpad;      // k rounded up to a multiple of 8 (gathered-x buffer only)
-  int32_t nfull;     // full weak chunks (8 columns, mma-fragment order)
-  int32_t ktail;     // columns of the ragged last chunk (k % 8), stored row-major
-  int32_t tail_bytes;// 64 * ktail * 2 rounded up to 16
+  int32_t nfull;     // full weak chunks
+  int32_t ktail;     // columns of the ragged last chunk (k % 8), stored unpadded
+  int32_t tail_bytes;// 128 * ktail * 2
   int32_t G;         // scale/zero groups per row
-  int64_t ss_bytes;  // bytes per super-step (all 32 lanes)
-  int64_t rb_bytes;  // bytes per row-block record (code units + weak units)
+  int64_t ss_bytes;  // bytes per super-step (all 128 rows)
+  int64_t rb_bytes;  // bytes per row-block record (super-steps + weak chunks)
   int64_t units_off, sz_off, widx_off, total;
 };
 
@@ -44,9 +57,9 @@ OWQ_HD Geo make_geo(int32_t M, int32_t K, int32_t bits, int32_t group, int32_t k
   g.kpad = (int32_t)cdiv(k, kWeakChunk) * kWeakChunk;
   g.nfull = k / kWeakChunk;
   g.ktail = k % kWeakChunk;
-  g.tail_bytes = (int32_t)cdiv((int64_t)kRowBlock * g.ktail * 2, 16) * 16;
+  g.tail_bytes = kRowBlock * g.ktail * 2;
   g.G = group ? (int32_t)cdiv(K, group) : 1;
-  g.ss_bytes = 32 * (bits == 3 ? 48 : 64);
+  g.ss_bytes = (int64_t)kRowBlock * words_per_row(bits) * 4;
   g.rb_bytes = (int64_t)g.nss * g.ss_bytes + (int64_t)g.nfull * kWeakChunkBytes + g.tail_bytes;
   g.units_off = kHeaderBytes;
   g.sz_off = g.units_off + (int64_t)g.nrb * g.rb_bytes;
@@ -95,7 +108,7 @@ OWQ_HD int64_t cta_of_item(const Geo& g, int64_t grid, int64_t item) {
 }
 
 // Stage sequence of one CTA: runs of at most `cap` items of one kind (code or
-// weak) inside one row-block.  Producer and consumers walk the same sequence.
+// weak) inside one row-block.  Every role of the CTA walks the same sequence.
 struct StageIter {
   int64_t rb;
   int32_t li, n_rb, nss, cap;
@@ -125,62 +138,29 @@ OWQ_HD int32_t stage_bytes(const Geo& g, int32_t li, int32_t n) {
   return (has_tail ? (n - 1) * kWeakChunkBytes + g.tail_bytes : n * kWeakChunkBytes);
 }
 
-// ---- bit map of one super-step -------------------------------------------------
-// Lane l = 4*gq + t (gq = l/4 "groupID", t = l%4) owns, for each of the 4 packets
-// s (mma k16 steps) of the super-step, 16 pairs P = 4*r + a (r = row-tile 0..3,
-// a = mma A register 0..3).  Pair (P, half) holds the code of
-//   row = 16*r + gq + 8*(a & 1),  col = 16*t + 4*s + 2*(a >> 1) + half
-// inside the row-block / super-step.  A packet is 3 (3-bit) or 4 (4-bit) 32-bit
-// words; word w of packet s is lane word n = s*WPP + w, stored at byte
-// (n/4)*512 + l*16 + (n%4)*4 of the super-step record (one LDS.128 per 4 words).
-OWQ_HD int words_per_packet(int bits) { return bits == 3 ? 3 : 4; }
+// ---- bit map of one row's super-step -------------------------------------------
+// Word w of row r inside the super-step record.
+OWQ_HD int64_t row_word_byte(int bits, int r, int w) {
+  return w < 4 ? (int64_t)r * 16 + w * 4 : 2048 + (int64_t)r * (words_per_row(bits) - 4) * 4 + (w - 4) * 4;
+}
 
-OWQ_HD int pair_row(int P, int gq) { return 16 * (P >> 2) + gq + 8 * (P & 1); }
-OWQ_HD int pair_col(int P, int t, int s, int half) { return 16 * t + 4 * s + 2 * ((P & 3) >> 1) + half; }
-
-// Location (word within packet, bit within word) of bit `bit` of the code in (P, half).
-//  3-bit: P 0..8  : word P/3, field at bit 3*(P%3)          (+16 for the high half)
-//         P 9..14 : word (P-9)/2, field at bit 9+3*((P-9)%2) (+16)
-//         P 15    : code bit j in word j at bit 15           (+16)
-//  4-bit: word P/4, field at bit 4*(P%4)                     (+16)
-OWQ_HD void code_bit_loc(int bits, int P, int half, int bit, int& word, int& pos) {
+// Location of bit `bit` of the code in pair j (columns 2j, 2j+1), half 0/1.
+//  3-bit: j < 30: word j/5, sub j%5: sub 0..2 -> field at 3*sub, sub 3..4 -> at
+//         9 + 3*(sub-3) (after >> 9 the field sits at 0 / 3); +16 for half 1.
+//         j = 30: code bit b in word b at bit 15 (+16);  j = 31: word 3+b.
+//  4-bit: word j/4, field at 4*(j%4) (+16).
+OWQ_HD void code_bit_loc(int bits, int j, int half, int bit, int& word, int& pos) {
   if (bits == 4) {
-    word = P >> 2;
-    pos = 4 * (P & 3) + bit + 16 * half;
-  } else if (P < 9) {
-    word = P / 3;
-    pos = 3 * (P % 3) + bit + 16 * half;
-  } else if (P < 15) {
-    word = (P - 9) / 2;
-    pos = 9 + 3 * ((P - 9) % 2) + bit + 16 * half;
+    word = j >> 2;
+    pos = 4 * (j & 3) + bit + 16 * half;
+  } else if (j < 30) {
+    word = j / 5;
+    const int sub = j % 5;
+    pos = (sub < 3 ? 3 * sub : 9 + 3 * (sub - 3)) + bit + 16 * half;
   } else {
-    word = bit;
+    word = (j - 30) * 3 + bit;
     pos = 15 + 16 * half;
   }
-}
-
-OWQ_HD int64_t lane_word_byte(int n, int lane) { return (int64_t)(n >> 2) * 512 + lane * 16 + (n & 3) * 4; }
-
-// ---- weak block ----------------------------------------------------------------
-// Chunk j (8 weak columns) of a row-block: lane l = 4*gq + t holds, for row-tile r,
-// two fp16x2 registers of the mma m16n8k8 A fragment:
-//   reg0 = (v[16r+gq][8j+2t], v[16r+gq][8j+2t+1]),  reg1 = rows + 8.
-// Byte offset inside the chunk: l*32 + r*8 + reg*4 (+ 2 for the odd column).
-// The ragged last chunk (k % 8 columns) is stored unpadded, row-major
-// [64][k % 8] fp16 (padded to 16 bytes), right after the full chunks.
-OWQ_HD int64_t weak_byte(int row_in_rb, int col_in_chunk) {
-  int r = row_in_rb >> 4, rem = row_in_rb & 15, gq = rem & 7, reg = rem >> 3;
-  int t = col_in_chunk >> 1, odd = col_in_chunk & 1;
-  int lane = gq * 4 + t;
-  return (int64_t)lane * 32 + r * 8 + reg * 4 + odd * 2;
-}
-
-// ---- scale / zero block --------------------------------------------------------
-// For (row-block, group): 64 rows x (s, z) fp16 pairs; row 16r + gq + 8h at
-// byte gq*32 + (2r + h)*4 (s in the low half, z in the high half).
-OWQ_HD int sz_byte(int row_in_rb) {
-  int r = row_in_rb >> 4, rem = row_in_rb & 15, gq = rem & 7, h = rem >> 3;
-  return gq * 32 + (2 * r + h) * 4;
 }
 
 struct BlobHeader {            // first 256 bytes of the blob

@@ -129,55 +129,53 @@ void write_blob(const Layer& L, uint8_t* blob) {
   h.nrb = g.nrb; h.nss = g.nss; h.kpad = g.kpad; h.nitems = owq::items_per_rb(g); h.G = g.G;
   h.total = g.total; h.sz_off = g.sz_off; h.widx_off = g.widx_off;
   std::memcpy(blob, &h, sizeof(h));
-  const int wpp = owq::words_per_packet(L.bits);
+  const int wpr = owq::words_per_row(L.bits);
 #pragma omp parallel for schedule(dynamic, 1)
   for (int rb = 0; rb < g.nrb; ++rb) {
     uint8_t* rec = blob + g.units_off + (int64_t)rb * g.rb_bytes;
     for (int ss = 0; ss < g.nss; ++ss) {
       uint8_t* ssrec = rec + (int64_t)ss * g.ss_bytes;
-      for (int lane = 0; lane < 32; ++lane) {
-        const int gq = lane >> 2, t = lane & 3;
-        for (int s = 0; s < 4; ++s) {
-          uint32_t words[4] = {0, 0, 0, 0};
-          for (int P = 0; P < 16; ++P)
+      for (int rr = 0; rr < owq::kRowBlock; ++rr) {
+        const int row = rb * owq::kRowBlock + rr;
+        uint32_t words[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (row < L.M) {
+          for (int j = 0; j < owq::kSuperStep / 2; ++j)
             for (int half = 0; half < 2; ++half) {
-              int row = rb * owq::kRowBlock + owq::pair_row(P, gq);
-              int col = ss * owq::kSuperStep + owq::pair_col(P, t, s, half);
-              uint32_t code = (row < L.M && col < L.K) ? L.codes[(size_t)row * L.K + col] : 0u;
+              const int col = ss * owq::kSuperStep + 2 * j + half;
+              const uint32_t code = col < L.K ? L.codes[(size_t)row * L.K + col] : 0u;
               for (int bit = 0; bit < L.bits; ++bit) {
                 if (!((code >> bit) & 1u)) continue;
                 int word, pos;
-                owq::code_bit_loc(L.bits, P, half, bit, word, pos);
+                owq::code_bit_loc(L.bits, j, half, bit, word, pos);
                 words[word] |= 1u << pos;
               }
             }
-          for (int w = 0; w < wpp; ++w)
-            std::memcpy(ssrec + owq::lane_word_byte(s * wpp + w, lane), &words[w], 4);
         }
+        for (int w = 0; w < wpr; ++w) std::memcpy(ssrec + owq::row_word_byte(L.bits, rr, w), &words[w], 4);
       }
     }
     uint8_t* weak = rec + (int64_t)g.nss * g.ss_bytes;
     for (int j = 0; j < g.nfull; ++j)
       for (int rr = 0; rr < owq::kRowBlock; ++rr)
         for (int c = 0; c < owq::kWeakChunk; ++c) {
-          int row = rb * owq::kRowBlock + rr, col = j * owq::kWeakChunk + c;
-          uint16_t v = row < L.M ? L.wval[(size_t)row * L.k + col] : 0;
-          std::memcpy(weak + (int64_t)j * owq::kWeakChunkBytes + owq::weak_byte(rr, c), &v, 2);
+          const int row = rb * owq::kRowBlock + rr, col = j * owq::kWeakChunk + c;
+          const uint16_t v = row < L.M ? L.wval[(size_t)row * L.k + col] : 0;
+          std::memcpy(weak + (int64_t)j * owq::kWeakChunkBytes + (rr * owq::kWeakChunk + c) * 2, &v, 2);
         }
     uint8_t* tail = weak + (int64_t)g.nfull * owq::kWeakChunkBytes;
     for (int rr = 0; rr < owq::kRowBlock; ++rr)
       for (int c = 0; c < g.ktail; ++c) {
-        int row = rb * owq::kRowBlock + rr, col = g.nfull * owq::kWeakChunk + c;
-        uint16_t v = row < L.M ? L.wval[(size_t)row * L.k + col] : 0;
+        const int row = rb * owq::kRowBlock + rr, col = g.nfull * owq::kWeakChunk + c;
+        const uint16_t v = row < L.M ? L.wval[(size_t)row * L.k + col] : 0;
         std::memcpy(tail + 2 * (rr * g.ktail + c), &v, 2);
       }
     for (int gi = 0; gi < g.G; ++gi) {
       uint8_t* sz = blob + g.sz_off + ((int64_t)rb * g.G + gi) * owq::kSZBlockBytes;
       for (int rr = 0; rr < owq::kRowBlock; ++rr) {
-        int row = rb * owq::kRowBlock + rr;
+        const int row = rb * owq::kRowBlock + rr;
         uint16_t pair[2] = {0, 0};
         if (row < L.M) { pair[0] = L.scale[(size_t)row * g.G + gi]; pair[1] = L.zero[(size_t)row * g.G + gi]; }
-        std::memcpy(sz + owq::sz_byte(rr), pair, 4);
+        std::memcpy(sz + 4 * rr, pair, 4);
       }
     }
   }
@@ -296,55 +294,48 @@ owq_status owq_blob_decode_host(const void* h_blob, size_t bytes, owq_shape* sha
   if (st != OWQ_OK) return st;
   const uint8_t* blob = (const uint8_t*)h_blob;
   if (shape_out) *shape_out = {h.M, h.K, h.bits, h.group, h.k};
-  const int wpp = owq::words_per_packet(h.bits);
+  const int wpr = owq::words_per_row(h.bits);
   for (int rb = 0; rb < g.nrb; ++rb) {
     const uint8_t* rec = blob + g.units_off + (int64_t)rb * g.rb_bytes;
-    if (codes) {
-      for (int ss = 0; ss < g.nss; ++ss)
-        for (int lane = 0; lane < 32; ++lane) {
-          const int gq = lane >> 2, t = lane & 3;
-          for (int s = 0; s < 4; ++s) {
-            uint32_t words[4];
-            for (int w = 0; w < wpp; ++w)
-              std::memcpy(&words[w], rec + (int64_t)ss * g.ss_bytes + owq::lane_word_byte(s * wpp + w, lane), 4);
-            for (int P = 0; P < 16; ++P)
-              for (int half = 0; half < 2; ++half) {
-                int row = rb * owq::kRowBlock + owq::pair_row(P, gq);
-                int col = ss * owq::kSuperStep + owq::pair_col(P, t, s, half);
-                if (row >= h.M || col >= h.K) continue;
-                uint32_t c = 0;
-                for (int bit = 0; bit < h.bits; ++bit) {
-                  int word, pos;
-                  owq::code_bit_loc(h.bits, P, half, bit, word, pos);
-                  c |= ((words[word] >> pos) & 1u) << bit;
-                }
-                codes[(size_t)row * h.K + col] = (uint8_t)c;
+    for (int rr = 0; rr < owq::kRowBlock; ++rr) {
+      const int row = rb * owq::kRowBlock + rr;
+      if (row >= h.M) continue;
+      if (codes) {
+        for (int ss = 0; ss < g.nss; ++ss) {
+          uint32_t words[8];
+          for (int w = 0; w < wpr; ++w)
+            std::memcpy(&words[w], rec + (int64_t)ss * g.ss_bytes + owq::row_word_byte(h.bits, rr, w), 4);
+          for (int j = 0; j < owq::kSuperStep / 2; ++j)
+            for (int half = 0; half < 2; ++half) {
+              const int col = ss * owq::kSuperStep + 2 * j + half;
+              if (col >= h.K) continue;
+              uint32_t c = 0;
+              for (int bit = 0; bit < h.bits; ++bit) {
+                int word, pos;
+                owq::code_bit_loc(h.bits, j, half, bit, word, pos);
+                c |= ((words[word] >> pos) & 1u) << bit;
               }
-          }
+              codes[(size_t)row * h.K + col] = (uint8_t)c;
+            }
         }
-    }
-    if (weak_val) {
-      const uint8_t* weak = rec + (int64_t)g.nss * g.ss_bytes;
-      for (int rr = 0; rr < owq::kRowBlock; ++rr)
+      }
+      if (weak_val) {
+        const uint8_t* weak = rec + (int64_t)g.nss * g.ss_bytes;
         for (int col = 0; col < h.k; ++col) {
-          int row = rb * owq::kRowBlock + rr;
-          if (row >= h.M) continue;
           const int j = col / owq::kWeakChunk, c = col % owq::kWeakChunk;
           const uint8_t* src = j < g.nfull
-              ? weak + (int64_t)j * owq::kWeakChunkBytes + owq::weak_byte(rr, c)
+              ? weak + (int64_t)j * owq::kWeakChunkBytes + (rr * owq::kWeakChunk + c) * 2
               : weak + (int64_t)g.nfull * owq::kWeakChunkBytes + 2 * (rr * g.ktail + c);
           std::memcpy(&weak_val[(size_t)row * h.k + col], src, 2);
         }
-    }
-    for (int gi = 0; gi < g.G; ++gi)
-      for (int rr = 0; rr < owq::kRowBlock; ++rr) {
-        int row = rb * owq::kRowBlock + rr;
-        if (row >= h.M) continue;
+      }
+      for (int gi = 0; gi < g.G; ++gi) {
         uint16_t pair[2];
-        std::memcpy(pair, blob + g.sz_off + ((int64_t)rb * g.G + gi) * owq::kSZBlockBytes + owq::sz_byte(rr), 4);
+        std::memcpy(pair, blob + g.sz_off + ((int64_t)rb * g.G + gi) * owq::kSZBlockBytes + 4 * rr, 4);
         if (scale) scale[(size_t)row * g.G + gi] = pair[0];
         if (zero) zero[(size_t)row * g.G + gi] = pair[1];
       }
+    }
   }
   if (weak_idx)
     for (int t = 0; t < h.k; ++t) std::memcpy(&weak_idx[t], blob + g.widx_off + 2 * t, 2);

@@ -59,6 +59,58 @@ __global__ void read_tma(const char* __restrict__ p, size_t bytes, int* out) {
   if (acc == 0x12345678) out[0] = acc;
 }
 
+
+template <int STAGES, int CHUNK>
+__global__ void read_tma_range(const char* __restrict__ p, size_t bytes, int* out) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) uint64_t bar[STAGES];
+  const size_t per = (bytes / gridDim.x) / 1024 * 1024;
+  const size_t beg = (size_t)blockIdx.x * per;
+  const int nchunks = (int)(per / CHUNK);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      uint32_t a = (uint32_t)__cvta_generic_to_shared(&bar[s]);
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" :: "r"(a));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  int acc = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES && s < nchunks; ++s) {
+      uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[s]);
+      uint32_t d = (uint32_t)__cvta_generic_to_shared(smem + s * CHUNK);
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" :: "r"(b), "r"(CHUNK));
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   :: "r"(d), "l"(p + beg + (size_t)s * CHUNK), "r"(CHUNK), "r"(b) : "memory");
+    }
+    for (int c = 0; c < nchunks; ++c) {
+      int s = c % STAGES; uint32_t ph = (c / STAGES) & 1;
+      uint32_t b = (uint32_t)__cvta_generic_to_shared(&bar[s]);
+      asm volatile("{ .reg .pred P; W: mbarrier.try_wait.parity.shared.b64 P, [%0], %1; @!P bra W; }" :: "r"(b), "r"(ph));
+      acc ^= *(volatile int*)(smem + s * CHUNK);
+      int nc = c + STAGES;
+      if (nc < nchunks) {
+        uint32_t d = (uint32_t)__cvta_generic_to_shared(smem + s * CHUNK);
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" :: "r"(b), "r"(CHUNK));
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     :: "r"(d), "l"(p + beg + (size_t)nc * CHUNK), "r"(CHUNK), "r"(b) : "memory");
+      }
+    }
+  }
+  if (acc == 0x12345678) out[0] = acc;
+}
+template <int ST, int CH, typename K>
+void run_range(K k, const char* p, size_t bytes, int* out, int sms, const char* name) {
+  cudaError_t e0 = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, ST * CH);
+  if (e0 != cudaSuccess) printf("attr: %s\n", cudaGetErrorString(e0));
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  k<<<sms, 32, ST * CH>>>(p, bytes, out); cudaDeviceSynchronize();
+  float best = 1e9;
+  for (int r = 0; r < 5; ++r) { cudaEventRecord(a); k<<<sms, 32, ST * CH>>>(p, bytes, out); cudaEventRecord(b); cudaEventSynchronize(b); float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms; }
+  printf("%s stages=%d chunk=%d bytes=%zu : %.2f us, %.1f GB/s [%s]\n", name, ST, CH, bytes, best * 1e3, bytes / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
   int dev = 0, sms = 0, l2 = 0, clk = 0, memclk = 0, busw = 0;
   CK(cudaGetDevice(&dev));
@@ -106,6 +158,13 @@ int main() {
     for (int r = 0; r < 48; ++r) read_ldg<<<sms * 8, 256>>>((const int4*)(p + (r % nb) * lb), lb / 16, out);
     cudaEventRecord(b); cudaEventSynchronize(b); cudaEventElapsedTime(&tot, a, b);
     printf("ldg 57MB rotated x48: %.2f us/launch, %.1f GB/s\n", tot * 1000 / 48, 48.0 * lb / tot / 1e6);
+  }
+  for (size_t mb : {57ul, 227ul, 1024ul}) {
+    size_t by = (mb << 20);
+    run_range<5, 36864>(read_tma_range<5, 36864>, p, by, out, sms, "tma-range");
+    run_range<4, 24576>(read_tma_range<4, 24576>, p, by, out, sms, "tma-range");
+    run_range<8, 24576>(read_tma_range<8, 24576>, p, by, out, sms, "tma-range");
+    run_range<6, 32768>(read_tma_range<6, 32768>, p, by, out, sms, "tma-range");
   }
   return 0;
 }

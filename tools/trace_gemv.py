@@ -14,22 +14,21 @@ x = torch.from_numpy(synth.activations(B, K, seed=2)).cuda()
 for _ in range(3):
     L(x)
 torch.cuda.synchronize()
-t = np.fromfile(path, dtype=np.uint64).reshape(3, -1, 64)[-1].astype(np.int64)
-live = t[:, 0] > 0
-t = t[live]
+t = np.fromfile(path, dtype=np.uint64).reshape(3, -1, 256)[-1].astype(np.int64)
+t = t[t[:, 0] > 0]
 t0 = t[:, 0].min()
-def q(col, name):
-    v = t[:, col]; v = v[v > 0]
-    if len(v): print(f" {name:24s} min {(v.min()-t0)/1e3:7.2f} med {(np.median(v)-t0)/1e3:7.2f} max {(v.max()-t0)/1e3:7.2f}  (n={len(v)})")
-print(f"{M}x{K} b{bits} CTAs={live.sum()} stages/CTA {t[:,63].min()}..{t[:,63].max()} (us from first CTA start)")
-q(0, "start"); q(1, "init done"); q(2, "first full")
-for kk in range(8): q(35 + kk, f"producer issue {kk}")
-for kk in [0, 1, 2, 3, 4, 8, 12, 16, 24, 31]: q(3 + kk, f"stage {kk} done")
-for c, n in zip(range(50, 57), ["fin in", "fin sync1", "fin partial st", "fin atomic", "fin sync2", "fin reads", "fin out"]): q(c, n)
-q(62, "end")
-iv = []
-for c in range(len(t)):
-    st = t[c, 3:3 + min(32, t[c, 63])]
-    st = st[st > 0]
-    iv += list(np.diff(st) / 1e3)
-if iv: print(f" stage interval us: p10 {np.percentile(iv,10):.3f} med {np.median(iv):.3f} p90 {np.percentile(iv,90):.3f}")
+def rel(v): return (v - t0) / 1e3
+print(f"{M}x{K} b{bits} CTAs={len(t)}  (us from first CTA start; median over CTAs)")
+print(f" start med {np.median(rel(t[:,0])):.2f}  fin-in {np.median(rel(t[:,50])):.2f}  fin-out {np.median(rel(t[:,56])):.2f}  end {np.median(rel(t[:,62])):.2f} max {rel(t[:,62]).max():.2f}")
+print(" stage  prod_issue  dec_full  dec_done  mma_done  epi_done")
+for kk in range(0, 16):
+    cols = [64 + kk, 192 + kk, 96 + kk, 128 + kk, 160 + kk]
+    vals = []
+    for c in cols:
+        v = t[:, c]; v = v[v > 0]
+        vals.append(f"{np.median(rel(v)):9.2f}" if len(v) else "        -")
+    print(f" {kk:5d} " + " ".join(vals))
+names = ["decode/full", "decode/aempty", "mma/afull", "mma/dempty", "epi/full", "epi/dfull", "prod/empty"]
+print(" wait cycles per CTA (sum over waiting warps' lane 0), mean:")
+for i, nme in enumerate(names):
+    print(f"   {nme:14s} {t[:, 10 + i].mean():12.0f}")
