@@ -43,8 +43,9 @@
  * its super-steps followed by its weak-column chunks (8 columns each; the
  * ragged last chunk unpadded), so any run of items is one contiguous TMA bulk
  * copy.  Inside a super-step each row's 64 codes are 6 (3-bit) or 8 (4-bit)
- * 32-bit words, pre-positioned so that one LOP3 with an fp16 exponent "magic"
- * yields two exact values 1024 + q*2^p.  DESIGN.md §5 gives the exact bit map;
+ * 32-bit words, pre-positioned so that one LOP3 (or SHF + LOP3) yields four
+ * consecutive codes as the bytes of one tcgen05 kind::i8 A-operand column.
+ * DESIGN.md §5 gives the exact bit map;
  * owq_unpack_codes / owq_blob_decode_host invert it.
  */
 #ifndef OWQ_H_
@@ -57,7 +58,7 @@
 extern "C" {
 #endif
 
-#define OWQ_LAYOUT_VERSION 2
+#define OWQ_LAYOUT_VERSION 3
 #define OWQ_MAX_BATCH 16
 
 typedef enum {

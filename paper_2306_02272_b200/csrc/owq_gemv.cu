@@ -1,28 +1,35 @@
-// owq_gemv.cu -- sm_100a kernel of the OWQ hot path (arXiv 2306.02272, P:114,
-// P:276): y = (zero-filled b-bit matrix) x + (fp16 weak columns) x[idx], one
-// fused launch, batch 1..16.
+// owq_gemv.cu -- sm_100a kernels of the OWQ hot path (arXiv 2306.02272, P:114,
+// P:276): y = diag(s) (Q - z) x + W_weak x[idx] with Q the zero-filled b-bit
+// code matrix, one fused launch (+ one tiny x-digit pass), batch 1..16.
+//
+// Arithmetic (exact up to the final fp32 scaling): the codes q are the u8 A
+// operand of tcgen05.mma kind::i8 as they are (no dequantisation);
+// x is split into 6 balanced int8 digits, x * 2^24 = sum_i d_i 256^i, which is
+// exact for every finite fp16 (its ulp is >= 2^-24 and |x| < 2^16), so
+//   sum_k q_k x_k = 2^-24 sum_i 256^i D_i,   D_i = sum_k q_k d_ik  (int32, exact)
+// and the zero point comes in through S = sum_k x_k 2^24 (int64, exact):
+//   y = s * 2^-24 * (sum_i 256^i D_i - z * S)   per row and scale group.
 //
 // Persistent CTA per SM, byte-balanced stream-K over "items" (a super-step =
 // 128 rows x 64 columns of codes, or a chunk of 8 weak columns).  Warp roles:
-//   producer (1 warp)   : one lane streams stages (runs of items + the matching
-//                         x columns + scale/zero blocks) HBM -> a shared-memory
-//                         ring with cp.async.bulk (TMA) and mbarriers.
-//   decode (DWG x 4)    : one thread per output row.  Codes -> exact fp16 (q - z)
-//                         pairs with one LOP3 ("magic" exponent 0x6400) + one
-//                         HFMA2 per two weights, written to a TMEM A-buffer with
-//                         tcgen05.st; x is re-laid into UMMA core matrices.
-//   MMA (1 warp per WG) : one lane issues tcgen05.mma kind::f16 M=128 N=16 K=16
-//                         (A from TMEM, B = x from shared memory, D fp32 in TMEM;
-//                         one D per warpgroup and scale group, ping-pong) and
-//                         tcgen05.commit -> mbarriers.  MMAs from several issuing
-//                         warps overlap; one issuer serialises at ~46 cycles per
-//                         instruction (tools/umma_tput.cu).
-//   epilogue (4 warps)  : reads D (tcgen05.ld), applies the fp32 scale of the
-//                         row/group, adds the fp16 weak columns x gathered
-//                         x[idx] on CUDA cores (the paper's separate dense fp16
-//                         GEMV, folded in), and writes y -- directly, or
-//                         through the stream-K fixup (last-arriving CTA sums the
-//                         pieces in a fixed order: deterministic).
+//   producer (1 warp)   : one lane streams stages (runs of items + the digit
+//                         tiles and digit sums of their columns + scale/zero
+//                         blocks) HBM/L2 -> a shared-memory ring with
+//                         cp.async.bulk (TMA) and mbarriers.
+//   decode (DWG x 4)    : one thread per output row: the row's 64 codes ->
+//                         16 words of 4 code bytes (LOP3 / SHF only, see
+//                         owq_layout.h), written to a TMEM slot with tcgen05.st.
+//   MMA (1 warp per WG) : one lane issues 2 tcgen05.mma kind::i8 M=128 N=NN K=32
+//                         per item (A = codes from TMEM, B = x digits from shared
+//                         memory, D s32 in TMEM; one D per warpgroup and scale
+//                         group, ping-pong) and tcgen05.commit -> mbarriers.
+//   epilogue (4 warps)  : reads D (tcgen05.ld), combines the digits and the zero
+//                         point exactly, applies the fp32 scale of the row/group,
+//                         adds the fp16 weak columns x gathered x[idx] on CUDA
+//                         cores (the paper's separate dense fp16 GEMV, P:276,
+//                         folded in), and writes y -- directly, or through the
+//                         stream-K fixup (last-arriving CTA sums the pieces in a
+//                         fixed order: deterministic).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -38,9 +45,14 @@
 
 namespace owq {
 
-constexpr int kMmaN = 16;                        // tcgen05 N (batch padded to 16)
-constexpr int kXcBytes = 8 * 2 * 128;            // x tile of one super-step in UMMA core matrices
-constexpr uint32_t kFp16Magic = 0x64006400u;     // fp16x2 (1024, 1024)
+constexpr int kDigits = 6;          // int8 digits per x value (base 256, balanced)
+
+// MMA N (digit rows of B) for a batch: 6 * B padded to a valid tcgen05 N
+static inline int mma_n_for(int B) {
+  const int r = kDigits * B;
+  return r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 96;
+}
+static inline int batch_pad(int B) { return (B + 1) & ~1; }   // digit-sum rows (16-byte aligned runs)
 
 struct Params {
   const uint8_t* blob;
@@ -48,19 +60,21 @@ struct Params {
   void* y;
   uint32_t* counters;
   float* partial;
+  const uint8_t* tiles;   // x digits, [nss][NN rows x 64 columns] in UMMA K-major core matrices
+  const long long* sums;  // [nss][Bp] sum over the super-step of x * 2^24
   Geo g;
-  int32_t B;
+  int32_t B, Bp;
   int32_t y_f32;
   int32_t nst;            // pipeline stages
   int32_t cap;            // items per stage
   int32_t code_bytes;     // stage region for codes / weak chunks
-  int32_t xraw_stride;    // bytes per raw x row in a stage (cap * 64 * 2)
+  int32_t tile_off;       // digit tiles inside a stage
+  int32_t sum_off;        // digit sums inside a stage
   int32_t sz_off;         // scale/zero blocks inside a stage
   int32_t stage_bytes;
   int64_t xK;             // row stride of x in elements
   int32_t group_log2;     // log2(group_size / 64)
   unsigned long long* trace;   // experiments only (OWQ_TRACE)
-  int32_t dbg;            // experiments only (OWQ_DEBUG): 1 no decode, 2 no TMEM store, 3 no MMA
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -131,11 +145,6 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
 __device__ __forceinline__ void named_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
-__device__ __forceinline__ uint32_t hfma2u(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 __device__ __forceinline__ unsigned long long gtime() {
@@ -151,20 +160,17 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
                : "memory");
 }
-__device__ __forceinline__ void tc_mma_f16(uint32_t d_t, uint32_t a_t, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_t, uint32_t a_t, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_t),
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_t),
       "r"(a_t), "l"(b_desc), "r"(idesc), "r"(acc));
 }
-__device__ __forceinline__ void tc_st32(uint32_t taddr, const uint32_t* r) {
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
-      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
-      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* d) {
@@ -181,94 +187,103 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
-// instruction descriptor: D f32, A/B f16, K-major, N = 16, M = 128
-constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kMmaN >> 3) << 17) | ((uint32_t)(kRowBlock >> 4) << 24);
 
-// (w & MASK) | magic in ONE LOP3 (magic held in a register)
-template <uint32_t MASK>
-__device__ __forceinline__ uint32_t ext(uint32_t w, uint32_t magic) {
-  uint32_t d;
-  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(w), "n"(MASK), "r"(magic));
-  return d;
+// instruction descriptor, kind::i8: D s32, A u8 (codes), B s8 (x digits), K-major, M = 128
+template <int NN>
+__host__ __device__ constexpr uint32_t idesc_i8() {
+  return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(NN >> 3) << 17) | ((uint32_t)(kRowBlock >> 4) << 24);
 }
 
-// Decode of one row's super-step (64 codes) into 32 fp16x2 exact (q - z) pairs.
-// 3-bit: pair j < 30 sits in word j/5 at bit 3*(j%5) (sub 0..2) or, after >> 9,
-// at 3*(j%5 - 3); pairs 30/31 gather bit 15/31 of words 0..2 / 3..5 (owq_layout.h).
+// Codes of one row's super-step -> 16 words, word c = codes of columns 4c..4c+3
+// as bytes (the bit map of owq_layout.h::code_bit_loc).
 template <int BITS>
-struct Decoder {
-  static constexpr int NP = BITS == 3 ? 3 : 2;       // distinct field positions p
-  // HFMA2 multiplier 2^-p and base 1024*2^-p for position index q
-  static __device__ __forceinline__ uint32_t mul(int q) {
-    if (BITS == 3) return q == 0 ? 0x3C003C00u : (q == 1 ? 0x30003000u : 0x24002400u);   // 1, 1/8, 1/64
-    return q == 0 ? 0x3C003C00u : 0x2C002C00u;                                          // 1, 1/16
-  }
-  static __device__ __forceinline__ uint32_t base(int q) {
-    if (BITS == 3) return q == 0 ? 0x64006400u : (q == 1 ? 0x58005800u : 0x4C004C00u);   // 1024, 128, 16
-    return q == 0 ? 0x64006400u : 0x54005400u;                                          // 1024, 64
-  }
-  static __device__ __forceinline__ constexpr int pidx(int j) {
-    return BITS == 3 ? (j < 30 ? ((j % 5) < 3 ? (j % 5) : (j % 5) - 3) : 2) : ((j & 3) & 1);
-  }
-  static __device__ __forceinline__ void run(const uint32_t* w, uint32_t mg, const uint32_t* cz, uint32_t* e) {
-    if (BITS == 3) {
-      constexpr uint32_t m0 = 0x00070007u, m3 = 0x00380038u, m6 = 0x01C001C0u, ml = 0x00400040u;
-      uint32_t v[6];
+__device__ __forceinline__ void decode_row(const uint32_t* w, uint32_t* o) {
+  if (BITS == 4) {
 #pragma unroll
-      for (int i = 0; i < 6; ++i) {
-        v[i] = w[i] >> 9;
-        e[5 * i + 0] = ext<m0>(w[i], mg);
-        e[5 * i + 1] = ext<m3>(w[i], mg);
-        e[5 * i + 2] = ext<m6>(w[i], mg);
-        e[5 * i + 3] = ext<m0>(v[i], mg);
-        e[5 * i + 4] = ext<m3>(v[i], mg);
-      }
-      e[30] = ext<ml>(v[0], mg) + ((v[1] & ml) << 1) + ((v[2] & ml) << 2);
-      e[31] = ext<ml>(v[3], mg) + ((v[4] & ml) << 1) + ((v[5] & ml) << 2);
-    } else {
-      constexpr uint32_t m0 = 0x000F000Fu, m4 = 0x00F000F0u;
+    for (int i = 0; i < 8; ++i) {
+      o[i] = w[i] & 0x0F0F0F0Fu;
+      o[8 + i] = (w[i] >> 4) & 0x0F0F0F0Fu;
+    }
+  } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t v = w[i] >> 8;
-        e[4 * i + 0] = ext<m0>(w[i], mg);
-        e[4 * i + 1] = ext<m4>(w[i], mg);
-        e[4 * i + 2] = ext<m0>(v, mg);
-        e[4 * i + 3] = ext<m4>(v, mg);
-      }
+    for (int i = 0; i < 6; ++i) {
+      o[i] = w[i] & 0x07070707u;
+      o[6 + i] = (w[i] >> 3) & 0x07070707u;
     }
 #pragma unroll
-    for (int j = 0; j < 32; ++j) e[j] = hfma2u(e[j], mul(pidx(j)), cz[pidx(j)]);   // exact q - z
+    for (int r = 0; r < 4; ++r)
+      o[12 + r] = ((w[r] >> 6) & 0x03030303u) | ((w[4 + (r >> 1)] >> (4 + (r & 1))) & 0x04040404u);
   }
-};
+}
 
-// x rows whose stride or base breaks 16-byte TMA alignment are first copied
-// into a zero-padded [B][Kp] buffer in the workspace (Kp = K rounded up to 64).
-__global__ void owq_pad_x_kernel(const __half* __restrict__ x, __half* __restrict__ xp, int B, int K, int Kp) {
-  const int64_t n = (int64_t)B * Kp;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(i / Kp), c = (int)(i - (int64_t)b * Kp);
-    xp[i] = c < K ? x[(int64_t)b * K + c] : __float2half(0.f);
+// ---- x -> int8 digits (one CTA per super-step) -----------------------------------
+// x * 2^24 = sum_{i<6} d_i 256^i with d_i in [-128, 127] (balanced base 256).
+__device__ __forceinline__ long long x_fixed(__half h) { return (long long)(__half2float(h) * 16777216.0f); }
+__device__ __forceinline__ int x_digit(long long X, int i) {
+  for (int j = 0; j < i; ++j) {
+    const int d = (int)(signed char)(X & 0xFF);
+    X = (X - d) >> 8;
+  }
+  return (int)(signed char)(X & 0xFF);
+}
+// tiles: [nss][NN*64] bytes; byte ((kc * NN/8 + nb) * 8 + r) * 16 + kk holds digit
+// row n = 8 nb + r (= 6 b + i), column k = 16 kc + kk of the super-step.
+__global__ void owq_x_digits_kernel(const __half* __restrict__ x, int64_t xK, int B, int Bp, int K, int NN,
+                                    uint8_t* __restrict__ tiles, long long* __restrict__ sums) {
+  const int ss = blockIdx.x;
+  const int nbk = NN / 8;
+  uint32_t* tile = reinterpret_cast<uint32_t*>(tiles + (int64_t)ss * NN * 64);
+  for (int p4 = threadIdx.x; p4 < NN * 16; p4 += blockDim.x) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int pos = p4 * 4 + t;
+      const int kk = pos & 15, r = (pos >> 4) & 7, blk = pos >> 7;
+      const int nb = blk % nbk, kc = blk / nbk;
+      const int n = nb * 8 + r;
+      const int64_t col = (int64_t)ss * kSuperStep + kc * 16 + kk;
+      int d = 0;
+      if (n < kDigits * B && col < K) d = x_digit(x_fixed(x[(int64_t)(n / kDigits) * xK + col]), n % kDigits);
+      word |= (uint32_t)(uint8_t)d << (8 * t);
+    }
+    tile[p4] = word;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int b = warp; b < Bp; b += blockDim.x >> 5) {
+    long long s = 0;
+    if (b < B)
+      for (int k = lane; k < kSuperStep; k += 32) {
+        const int64_t col = (int64_t)ss * kSuperStep + k;
+        if (col < K) s += x_fixed(x[(int64_t)b * xK + col]);
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) sums[(int64_t)ss * Bp + b] = s;
   }
 }
 
 // group of code item li (row-block relative super-step index)
 __device__ __forceinline__ int group_of(const Params& p, int li) { return p.g.group ? (li >> p.group_log2) : 0; }
 
-template <int BITS, int DWG, bool X1>
+// Per MMA-N class: decode warpgroups, TMEM A slots per warpgroup, largest batch.
+template <int BITS, int NN>
 struct Cfg {
+  static constexpr int DWG = NN <= 32 ? 4 : 2;
+  static constexpr int kR = NN <= 32 ? 4 : (NN == 64 ? 8 : 4);
+  static constexpr int kMaxB = NN == 8 ? 1 : NN == 16 ? 2 : NN == 32 ? 5 : NN == 64 ? 10 : 16;
   static constexpr int kDecodeWarps = 4 * DWG;            // DWG decode warpgroups
   static constexpr int kEpiWarp0 = kDecodeWarps;          // 4 epilogue warps (warp % 4 = TMEM lane quarter)
   static constexpr int kMmaWarp0 = kEpiWarp0 + 4;         // one MMA-issuer warp per warpgroup
   static constexpr int kProdWarp = kMmaWarp0 + DWG;
   static constexpr int kWarps = kProdWarp + 1;
   static constexpr int kThreads = kWarps * 32;
-  static constexpr int kIPB = 2;                          // super-steps per A buffer (one publish)
-  static constexpr int kTmemCols = 512;                   // A: DWG*2*kIPB*32, D: DWG*2*16
-  static constexpr int kACols = kIPB * 32;
-  static constexpr int kDCol0 = DWG * 2 * kACols;
-  // per stage: decode + epilogue warps arrive; with X1 each MMA warp also commits
-  // (its MMAs read x from the stage)
-  static constexpr int kEmptyCount = kDecodeWarps + 4 + (X1 ? DWG : 0);
+  static constexpr int kTmemCols = 512;
+  static constexpr int kACols = kSuperStep / 4;           // 16 TMEM columns (4 code bytes each) per item
+  static constexpr int kDCol0 = DWG * kR * kACols;        // then D: [DWG][2] x NN columns
+  static_assert(kDCol0 + DWG * 2 * NN <= kTmemCols, "TMEM budget");
+  static_assert(kMaxB * kDigits <= NN, "digit rows");
+  // per stage: decode + epilogue warps arrive, each MMA warp commits (B is read from the stage)
+  static constexpr int kEmptyCount = kDecodeWarps + 4 + DWG;
 };
 
 // Segments of a code stage: maximal runs of items of one scale group.  For
@@ -302,22 +317,22 @@ __device__ __forceinline__ void share(int n, int w, int dwg, int& lo, int& hi) {
   if (lo > n) lo = n;
 }
 
-template <int BITS, int DWG, bool X1>
-__global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kernel(const Params p) {
-  using C = Cfg<BITS, DWG, X1>;
+template <int BITS, int NN>
+__global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(const Params p) {
+  using C = Cfg<BITS, NN>;
+  constexpr int DWG = C::DWG, R = C::kR, MAXB = C::kMaxB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geo& g = p.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NST = p.nst;
   uint8_t* ring = smem;
-  uint8_t* xc = smem + (size_t)NST * p.stage_bytes;                      // [DWG][2][kIPB][kXcBytes]
-  __half* xw = reinterpret_cast<__half*>(xc + DWG * 2 * C::kIPB * kXcBytes);   // [B][kpad]
+  __half* xw = reinterpret_cast<__half*>(smem + (size_t)NST * p.stage_bytes);   // [B][kpad] x at the weak columns
   uint64_t* bars = reinterpret_cast<uint64_t*>(xw + (((size_t)p.B * g.kpad + 7) & ~(size_t)7));
   uint64_t* full = bars;
   uint64_t* empty = full + NST;
-  uint64_t* afull = empty + NST;       // [DWG][2]  A buffer + x tile written (4 warps)
-  uint64_t* aempty = afull + 2 * DWG;  // [DWG][2]  MMA done reading them
-  uint64_t* dfull = aempty + 2 * DWG;  // [DWG][2]  group accumulator complete
+  uint64_t* afull = empty + NST;       // [DWG][R]  A item slot written (4 warps)
+  uint64_t* aempty = afull + DWG * R;  // [DWG][R]  MMA done reading it
+  uint64_t* dfull = aempty + DWG * R;  // [DWG][2]  group accumulator complete
   uint64_t* dempty = dfull + 2 * DWG;  // [DWG][2]  epilogue drained it
   unsigned long long* wprof = reinterpret_cast<unsigned long long*>(dempty + 2 * DWG);   // [8] wait cycles
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wprof + 8);
@@ -333,9 +348,8 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); }
-    for (int i = 0; i < 2 * DWG; ++i) {
-      mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4);
-    }
+    for (int i = 0; i < DWG * R; ++i) { mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); }
+    for (int i = 0; i < 2 * DWG; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int i = 0; i < 8; ++i) wprof[i] = 0ull;
   }
@@ -344,37 +358,15 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
                  "n"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  // x tiles start zeroed: rows >= B of the UMMA B operand are never written
-  for (int i = threadIdx.x; i < DWG * 2 * C::kIPB * kXcBytes / 16; i += C::kThreads)
-    reinterpret_cast<uint4*>(xc)[i] = make_uint4(0, 0, 0, 0);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int n_rb = items_per_rb(g);
+  const uint32_t tile_bytes = (uint32_t)NN * kSuperStep;
+  const uint32_t sum_bytes = (uint32_t)p.Bp * 8u;
 
-  if (p.dbg == 6 && warp != C::kProdWarp) {
-    if (warp < C::kEpiWarp0 + 4 || warp >= C::kMmaWarp0) {
-      StageIter it;
-      it.init(g, i0, i1, p.cap);
-      int64_t srb;
-      int32_t sli, n;
-      int s = 0;
-      uint32_t ph = 0;
-      const bool is_mma = warp >= C::kMmaWarp0;
-      while ((n = it.next(srb, sli)) > 0) {
-        if (!is_mma) {
-          mbar_wait(&full[s], ph);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
-        } else if (X1 && lane == 0) {
-          mbar_wait(&full[s], ph);
-          mbar_arrive(&empty[s]);
-        }
-        if (++s == NST) { s = 0; ph ^= 1u; }
-      }
-    }
-  } else if (warp == C::kProdWarp) {
+  if (warp == C::kProdWarp) {
     // ==================================================================== producer
     if (lane == 0) {
       const uint64_t pol = evict_first_policy(), pol_x = evict_last_policy();
@@ -386,51 +378,16 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
       uint32_t ph = 0;
       while ((n = it.next(srb, sli)) > 0) {
         if (k >= NST) mbar_wait_p(&empty[s], ph ^ 1u, WP ? WP + 6 : nullptr);
-        if (p.dbg == 4 || p.dbg == 5) {   // experiments: plain bulk copies (no L2 hint) / codes only
-          uint8_t* st = ring + (size_t)s * p.stage_bytes;
-          const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
-          uint32_t tot = cbytes;
-          int64_t col0 = (int64_t)sli * kSuperStep;
-          int xcols = 0, gi0 = 0, ngrp = 0;
-          if (sli < g.nss && p.dbg == 4) {
-            const int ncols = n * kSuperStep;
-            xcols = (int)(p.xK - col0 < ncols ? p.xK - col0 : ncols);
-            gi0 = group_of(p, sli);
-            ngrp = group_of(p, sli + n - 1) - gi0 + 1;
-            tot += (uint32_t)(p.B * xcols * 2 + ngrp * kSZBlockBytes);
-          }
-          mbar_expect_tx(&full[s], tot);
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                           smem_addr(st)), "l"(p.blob + g.units_off + item_offset(g, srb, sli)), "r"(cbytes), "r"(smem_addr(&full[s])) : "memory");
-          if (xcols) {
-            for (int b = 0; b < p.B; ++b)
-              asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                               smem_addr(st + p.code_bytes + b * p.xraw_stride)), "l"(p.x + (int64_t)b * p.xK + col0), "r"(xcols * 2), "r"(smem_addr(&full[s])) : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                             smem_addr(st + p.sz_off)), "l"(p.blob + g.sz_off + (srb * g.G + gi0) * kSZBlockBytes), "r"(ngrp * kSZBlockBytes), "r"(smem_addr(&full[s])) : "memory");
-          }
-          ++k;
-          if (++s == NST) { s = 0; ph ^= 1u; }
-          continue;
-        }
         if (p.trace && k < 32) p.trace[cta * 256 + 64 + k] = gtime();
         uint8_t* st = ring + (size_t)s * p.stage_bytes;
         const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
         if (sli < g.nss) {
-          const int64_t col0 = (int64_t)sli * kSuperStep;
-          const int ncols = n * kSuperStep;
-          const int xcols = (int)(p.xK - col0 < ncols ? p.xK - col0 : ncols);
-          if (xcols < ncols)   // zero the columns past K (their codes meet x = 0)
-            for (int b = 0; b < p.B; ++b)
-              for (int c = xcols; c < ncols; ++c)
-                reinterpret_cast<__half*>(st + p.code_bytes + b * p.xraw_stride)[c] = __float2half(0.f);
           const int gi0 = group_of(p, sli);
           const int ngrp = group_of(p, sli + n - 1) - gi0 + 1;
-          mbar_expect_tx(&full[s], cbytes + (uint32_t)(p.B * xcols * 2 + ngrp * kSZBlockBytes));
+          mbar_expect_tx(&full[s], cbytes + (uint32_t)n * (tile_bytes + sum_bytes) + (uint32_t)(ngrp * kSZBlockBytes));
           bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
-          for (int b = 0; b < p.B; ++b)
-            bulk_g2s(st + p.code_bytes + b * p.xraw_stride, p.x + (int64_t)b * p.xK + col0, (uint32_t)(xcols * 2),
-                     &full[s], pol_x);
+          bulk_g2s(st + p.tile_off, p.tiles + (int64_t)sli * tile_bytes, (uint32_t)n * tile_bytes, &full[s], pol_x);
+          bulk_g2s(st + p.sum_off, p.sums + (int64_t)sli * p.Bp, (uint32_t)n * sum_bytes, &full[s], pol_x);
           bulk_g2s(st + p.sz_off, p.blob + g.sz_off + (srb * g.G + gi0) * kSZBlockBytes,
                    (uint32_t)(ngrp * kSZBlockBytes), &full[s], pol);
         } else {
@@ -443,22 +400,15 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
     }
   } else if (warp < C::kDecodeWarps) {
     // ==================================================================== decode
+    // Warpgroup wg decodes a contiguous share of every code stage, one item
+    // (128 rows x 64 codes) into one TMEM slot of its R-slot ring, and publishes
+    // each item to its MMA warp (afull); the slot comes back through aempty.
     const int wg = warp >> 2, q = warp & 3;
     const int row = q * 32 + lane;                      // TMEM lane / row inside the row-block
-    const int wt = threadIdx.x & 127;                   // thread index inside the warpgroup
-    using D = Decoder<BITS>;
-    uint32_t magic;
-    asm volatile("mov.b32 %0, %1;" : "=r"(magic) : "n"(kFp16Magic));
-    uint32_t cz[D::NP];
-#pragma unroll
-    for (int i = 0; i < D::NP; ++i) cz[i] = 0u;
-    int64_t key_rb = -1;
-    int key_gi = -1;
-    uint32_t acnt = 0;          // A-buffer uses
-    const uint32_t xc_wg = smem_addr(xc) + (uint32_t)(wg * 2 * C::kIPB * kXcBytes);
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    const int xb_ = wt >> 3, xkc = wt & 7;
-    const bool xthr = wt < p.B * 8;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * R * C::kACols);
+    const uint32_t ss = (uint32_t)g.ss_bytes;
+    constexpr uint32_t kHiStride = BITS == 3 ? 8u : 16u;   // words 4.. of a row
+    uint32_t slot = 0, rnd = 0;                         // ring position, completed rounds
     StageIter it;
     it.init(g, i0, i1, p.cap);
     int64_t srb;
@@ -469,61 +419,35 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
     while ((n = it.next(srb, sli)) > 0) {
       mbar_wait_p(&full[s], ph, WP ? WP + 0 : nullptr);
       if (p.trace && warp == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 192 + kst] = gtime();
-      const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
       if (sli < g.nss) {
-        const int gi0 = group_of(p, sli);
+        const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
         int lo, hi;
         share(n, wg, DWG, lo, hi);
-        for (int pa = lo; pa < hi; pa += C::kIPB) {
-          const uint32_t buf = acnt & 1u, aph = (acnt >> 1) & 1u;
-          if (acnt >= 2) mbar_wait_p(&aempty[wg * 2 + buf], aph ^ 1u, WP ? WP + 1 : nullptr);
-          ++acnt;
-          tc_fence_after();
-          const int pe = pa + C::kIPB < hi ? pa + C::kIPB : hi;
-          for (int pi = pa; pi < pe; ++pi) {
-            const int gi = group_of(p, sli + pi);
-            if (srb != key_rb || gi != key_gi) {
-              const uint32_t sz = lds32(sbase + p.sz_off + (gi - gi0) * kSZBlockBytes + row * 4);
-              const __half2 zz = __high2half2(u2h(sz));
-#pragma unroll
-              for (int i = 0; i < D::NP; ++i) cz[i] = h2u(__hneg2(__hadd2(u2h(D::base(i)), zz)));
-              key_rb = srb;
-              key_gi = gi;
-            }
-            const uint32_t ssb = sbase + (uint32_t)(pi * g.ss_bytes);
-            uint32_t w[8];
-            {
-              const uint4 a = lds128(ssb + row * 16);
-              w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
-              if (BITS == 3) {
-                const uint2 b = lds64(ssb + 2048 + row * 8);
-                w[4] = b.x; w[5] = b.y;
-              } else {
-                const uint4 b = lds128(ssb + 2048 + row * 16);
-                w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
-              }
-            }
-            uint4 xpiece = make_uint4(0, 0, 0, 0);
-            if (!X1 && xthr) xpiece = lds128(sbase + p.code_bytes + xb_ * p.xraw_stride + (pi * kSuperStep + xkc * 8) * 2);
-            uint32_t e[32];
-            if (p.dbg == 1) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) e[j] = w[j & 7];
+        uint32_t a_lo = sbase + (uint32_t)lo * ss + (uint32_t)row * 16u;
+        uint32_t a_hi = sbase + (uint32_t)lo * ss + 2048u + (uint32_t)row * kHiStride;
+        for (int pi = lo; pi < hi; ++pi, a_lo += ss, a_hi += ss) {
+          uint32_t w[8];
+          {
+            const uint4 a = lds128(a_lo);
+            w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+            if (BITS == 3) {
+              const uint2 b = lds64(a_hi);
+              w[4] = b.x; w[5] = b.y;
             } else {
-              D::run(w, magic, cz, e);
+              const uint4 b = lds128(a_hi);
+              w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
             }
-            const int slot_i = pi - pa;   // item slot inside the A buffer
-            if (p.dbg != 2) tc_st32(trow + (uint32_t)((wg * 2 + buf) * C::kACols + slot_i * 32), e);
-            else if ((e[0] ^ e[7] ^ e[13] ^ e[31]) == 0x12345678u) asm volatile("trap;");
-            if (!X1 && xthr)
-              sts128(xc_wg + (uint32_t)((buf * C::kIPB + slot_i) * kXcBytes + (xkc * 2 + (xb_ >> 3)) * 128 + (xb_ & 7) * 16),
-                     xpiece);
           }
+          uint32_t o[16];
+          decode_row<BITS>(w, o);
+          if (rnd) mbar_wait_p(&aempty[wg * R + slot], (rnd - 1u) & 1u, WP ? WP + 1 : nullptr);
+          tc_fence_after();
+          tc_st16(trow + slot * (uint32_t)C::kACols, o);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          if (!X1) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // x tiles -> async proxy (MMA)
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&afull[wg * 2 + buf]);
+          if (lane == 0) mbar_arrive(&afull[wg * R + slot]);
+          if (++slot == (uint32_t)R) { slot = 0; ++rnd; }
         }
       }
       __syncwarp();
@@ -536,9 +460,10 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
     // ==================================================================== MMA issue (one warp per warpgroup)
     const int wg = warp - C::kMmaWarp0;
     if (lane == 0) {
-      uint32_t acnt = 0, dcnt = 0;
+      uint32_t slot = 0, rnd = 0, dcnt = 0;
       bool open = false;          // D[dcnt & 1] holds a partial group sum
-      const uint32_t xc_wg = smem_addr(xc) + (uint32_t)(wg * 2 * C::kIPB * kXcBytes);
+      const uint32_t a_wg = tmem + (uint32_t)(wg * R * C::kACols);
+      constexpr uint32_t kLbo = (NN / 8) * 128;        // K-adjacent core matrices
       StageIter it;
       it.init(g, i0, i1, p.cap);
       int64_t crb, nrb = -1;
@@ -548,37 +473,27 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
       while (cn > 0) {
         const int32_t nn = it.next(nrb, nli);
         if (cli < g.nss) {
-          const uint32_t sx = smem_addr(ring + (size_t)s * p.stage_bytes) + p.code_bytes;   // raw x (X1)
+          const uint32_t stile = smem_addr(ring + (size_t)s * p.stage_bytes) + (uint32_t)p.tile_off;
           int lo, hi;
           share(cn, wg, DWG, lo, hi);
-          uint32_t buf = 0;
           for (int pa = 0; pa < cn;) {
             const Seg sg = segment(p, pa, cn, cli, crb, nn, nrb, nli);
             const int a0 = sg.pa > lo ? sg.pa : lo, a1 = sg.pb + 1 < hi ? sg.pb + 1 : hi;
             for (int pi = a0; pi < a1; ++pi) {
-              const int slot_i = (pi - lo) % C::kIPB;
-              if (slot_i == 0) {   // first item of an A buffer: wait for its publish
-                buf = acnt & 1u;
-                const uint32_t aph = (acnt >> 1) & 1u;
-                ++acnt;
-                mbar_wait_p(&afull[wg * 2 + buf], aph, WP ? WP + 2 : nullptr);
-                tc_fence_after();
-              }
+              mbar_wait_p(&afull[wg * R + slot], rnd & 1u, WP ? WP + 2 : nullptr);
+              tc_fence_after();
               const uint32_t dbuf = dcnt & 1u;
               if (!open && dcnt >= 2) mbar_wait_p(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u, WP ? WP + 3 : nullptr);
-              const uint32_t a_t = tmem + (uint32_t)((wg * 2 + buf) * C::kACols + slot_i * 32);
-              const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * kMmaN);
+              const uint32_t a_t = a_wg + slot * (uint32_t)C::kACols;
+              const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * NN);
+              const uint32_t tb = stile + (uint32_t)pi * tile_bytes;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                if (p.dbg == 3) break;
-                // X1: core matrix row 0 = x[16j + 8c ..], rows 1..7 read the following
-                // chunks (finite, they only feed D columns 1..15 which are ignored)
-                const uint64_t bd = X1 ? umma_desc(sx + (uint32_t)(pi * kSuperStep * 2 + j * 32), 16, 0)
-                                       : umma_desc(xc_wg + (buf * C::kIPB + slot_i) * kXcBytes + j * 512, 256, 128);
-                tc_mma_f16(d_t, a_t + 8 * j, bd, kIdesc, (open || j > 0) ? 1u : 0u);
-              }
+              for (int j = 0; j < 2; ++j)   // K = 32 columns each: TMEM columns 8j.., core-matrix K-chunks 2j, 2j+1
+                tc_mma_i8(d_t, a_t + 8 * j, umma_desc(tb + j * 2 * kLbo, kLbo, 128), idesc_i8<NN>(),
+                          (open || j > 0) ? 1u : 0u);
               open = true;
-              if (slot_i == C::kIPB - 1 || pi + 1 == hi) tc_commit(&aempty[wg * 2 + buf]);   // buffer consumed
+              tc_commit(&aempty[wg * R + slot]);   // slot consumed once these MMAs complete
+              if (++slot == (uint32_t)R) { slot = 0; ++rnd; }
             }
             if (sg.ends && open) {
               tc_commit(&dfull[wg * 2 + (dcnt & 1u)]);
@@ -588,7 +503,7 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
             pa = sg.pb + 1;
           }
         }
-        if (X1) tc_commit(&empty[s]);   // the stage's x is free once these MMAs completed
+        tc_commit(&empty[s]);   // the stage's digit tiles are free once these MMAs completed
         if (p.trace && wg == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
         ++kst;
         if (++s == NST) s = 0;
@@ -610,9 +525,11 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
       }
     }
     named_sync(2, 128);
-    float tot[kMmaN];
+    constexpr double kPow256[6] = {1.0, 256.0, 65536.0, 16777216.0, 4294967296.0, 1099511627776.0};
+    float tot[MAXB];
+    long long sacc[MAXB];                                // sum over the open group's items of x * 2^24
 #pragma unroll
-    for (int b = 0; b < kMmaN; ++b) tot[b] = 0.f;
+    for (int b = 0; b < MAXB; ++b) { tot[b] = 0.f; sacc[b] = 0; }
     uint32_t dcnt[DWG];
 #pragma unroll
     for (int w = 0; w < DWG; ++w) dcnt[w] = 0;
@@ -639,21 +556,39 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
             share(cn, w, DWG, lo, hi);
             if (lo <= sg.pb && hi > sg.pa) part |= 1u << w;
           }
-          if (sg.ends) {
-            const float s_g = __low2float(u2h(lds32(sbase + p.sz_off + (sg.gi - gi0) * kSZBlockBytes + row * 4)));
-            float sum[kMmaN];
+          for (int pi = sg.pa; pi <= sg.pb; ++pi) {
+            const uint32_t sp = sbase + (uint32_t)p.sum_off + (uint32_t)pi * sum_bytes;
 #pragma unroll
-            for (int b = 0; b < kMmaN; ++b) sum[b] = 0.f;
+            for (int b = 0; b < MAXB; ++b)
+              if (b < p.B) {
+                const uint2 v = lds64(sp + b * 8);
+                sacc[b] += (long long)(((unsigned long long)v.y << 32) | v.x);
+              }
+          }
+          if (sg.ends) {
+            const __half2 szv = u2h(lds32(sbase + p.sz_off + (sg.gi - gi0) * kSZBlockBytes + row * 4));
+            const float s_g = __low2float(szv);
+            const double z_g = (double)__high2float(szv);
+            double dacc[MAXB];
+#pragma unroll
+            for (int b = 0; b < MAXB; ++b) dacc[b] = 0.0;
 #pragma unroll
             for (int w = 0; w < DWG; ++w) {
               if (part & (1u << w)) {   // fixed order over warpgroups: deterministic
                 const uint32_t dbuf = dcnt[w] & 1u;
                 mbar_wait_p(&dfull[w * 2 + dbuf], (dcnt[w] >> 1) & 1u, WP ? WP + 5 : nullptr);
                 tc_fence_after();
-                uint32_t d[kMmaN];
-                tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * kMmaN), d);
+                const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * NN);
 #pragma unroll
-                for (int b = 0; b < kMmaN; ++b) sum[b] += __uint_as_float(d[b]);
+                for (int c16 = 0; c16 < (MAXB * kDigits + 15) / 16; ++c16) {
+                  uint32_t d[16];
+                  tc_ld16(tcol + 16 * c16, d);
+#pragma unroll
+                  for (int j = 0; j < 16; ++j) {
+                    const int col = 16 * c16 + j, b = col / kDigits, i = col % kDigits;
+                    if (b < MAXB) dacc[b] += (double)(int)d[j] * kPow256[i];
+                  }
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&dempty[w * 2 + dbuf]);
@@ -661,7 +596,10 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
               }
             }
 #pragma unroll
-            for (int b = 0; b < kMmaN; ++b) tot[b] = fmaf(s_g, sum[b], tot[b]);
+            for (int b = 0; b < MAXB; ++b) {
+              tot[b] = fmaf(s_g, (float)((dacc[b] - z_g * (double)sacc[b]) * 5.9604644775390625e-08), tot[b]);
+              sacc[b] = 0;
+            }
             part = 0;
           }
           pa = sg.pb + 1;
@@ -686,7 +624,7 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
             for (int c = 0; c < 8; ++c) v[c] = c < g.ktail ? __half2float(tl[row * g.ktail + c]) : 0.f;
           }
 #pragma unroll
-          for (int b = 0; b < kMmaN; ++b) {
+          for (int b = 0; b < MAXB; ++b) {
             if (b < p.B) {
               const uint4 xv = *reinterpret_cast<const uint4*>(xw + b * g.kpad + gch * kWeakChunk);
               const uint32_t xwv[4] = {xv.x, xv.y, xv.z, xv.w};
@@ -717,7 +655,7 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
         if (whole) {
           if (grow < g.M) {
 #pragma unroll
-            for (int b = 0; b < kMmaN; ++b)
+            for (int b = 0; b < MAXB; ++b)
               if (b < p.B) {
                 if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = tot[b];
                 else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(tot[b]);
@@ -725,7 +663,7 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
           }
         } else {
 #pragma unroll
-          for (int b = 0; b < kMmaN; ++b)
+          for (int b = 0; b < MAXB; ++b)
             if (b < p.B) __stcg(&p.partial[((crb + cta) * p.B + b) * kRowBlock + row], tot[b]);
           // pieces = CTAs cta_of(first item) .. cta_of(last item) (none is empty)
           const int64_t c_first = cta_of_item(g, grid, ifirst), c_last = cta_of_item(g, grid, ilast);
@@ -753,7 +691,7 @@ __global__ void __launch_bounds__(Cfg<BITS, DWG, X1>::kThreads, 1) owq_gemv_kern
           named_sync(2, 128);
         }
 #pragma unroll
-        for (int b = 0; b < kMmaN; ++b) tot[b] = 0.f;
+        for (int b = 0; b < MAXB; ++b) tot[b] = 0.f;
         if (p.trace && et == 0) p.trace[cta * 256 + 56] = gtime();
       }
       crb = nrb;
@@ -785,18 +723,17 @@ __global__ void owq_unpack_codes_kernel(const uint8_t* blob, Geo g, uint8_t* cod
   const uint8_t* rec = blob + g.units_off + (int64_t)rb * g.rb_bytes + (int64_t)ss * g.ss_bytes;
   uint32_t w[8];
   for (int i = 0; i < words_per_row(g.bits); ++i) w[i] = *reinterpret_cast<const uint32_t*>(rec + row_word_byte(g.bits, rr, i));
-  for (int j = 0; j < kSuperStep / 2; ++j)
-    for (int half = 0; half < 2; ++half) {
-      const int64_t col = (int64_t)ss * kSuperStep + 2 * j + half;
-      if (col >= g.K) continue;
-      uint32_t c = 0;
-      for (int bit = 0; bit < g.bits; ++bit) {
-        int word, pos;
-        code_bit_loc(g.bits, j, half, bit, word, pos);
-        c |= ((w[word] >> pos) & 1u) << bit;
-      }
-      codes[row * g.K + col] = (uint8_t)c;
+  for (int cc = 0; cc < kSuperStep; ++cc) {
+    const int64_t col = (int64_t)ss * kSuperStep + cc;
+    if (col >= g.K) continue;
+    uint32_t c = 0;
+    for (int bit = 0; bit < g.bits; ++bit) {
+      int word, pos;
+      code_bit_loc(g.bits, cc, bit, word, pos);
+      c |= ((w[word] >> pos) & 1u) << bit;
     }
+    codes[row * g.K + col] = (uint8_t)c;
+  }
 }
 
 // ---------------------------------------------------------------- host side
@@ -851,37 +788,47 @@ static owq_status check_blob_cached(const owq_shape* s, const void* d_packed, Ge
   return st;
 }
 
-// Workspace: [counters nrb u32][partials (nrb + grid) x B x 128 f32][x pad B x Kp f16]
+// Workspace: [counters nrb u32][partials (nrb + grid) x B x 128 f32]
+//            [x digit tiles nss x NN x 64 B][x digit sums nss x Bp x 8 B]
 static size_t ws_counters(const Geo& g) { return ((size_t)g.nrb * 4 + 255) / 256 * 256; }
 static size_t ws_partials(const Geo& g, int B, int64_t G) {
   return ((size_t)(g.nrb + G) * B * kRowBlock * 4 + 255) / 256 * 256;
 }
+static size_t ws_tiles(const Geo& g, int B) { return (size_t)g.nss * mma_n_for(B) * kSuperStep; }
+static size_t ws_sums(const Geo& g, int B) { return (size_t)g.nss * batch_pad(B) * 8; }
 static size_t ws_bytes_for(const Geo& g, int B, int64_t G) {
-  return ws_counters(g) + ws_partials(g, B, G) + (size_t)B * g.nss * kSuperStep * 2;
+  return ws_counters(g) + ws_partials(g, B, G) + ws_tiles(g, B) + ws_sums(g, B);
 }
 
-template <int BITS, int DWG, bool X1>
+template <int BITS, int NN>
 static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
-  using C = Cfg<BITS, DWG, X1>;
+  using C = Cfg<BITS, NN>;
   Params p = p0;
-  p.cap = DWG * (BITS == 3 ? 4 : 2);
-  p.code_bytes = (int32_t)std::max<int64_t>((int64_t)p.cap * p.g.ss_bytes, (int64_t)p.cap * kWeakChunkBytes);
-  p.xraw_stride = p.cap * kSuperStep * 2;
-  p.sz_off = p.code_bytes + p.B * p.xraw_stride;
-  const int sz_blocks = p.g.group ? (int)(p.cap * kSuperStep / p.g.group + 2) : 1;
-  p.stage_bytes = (p.sz_off + sz_blocks * kSZBlockBytes + 127) / 128 * 128;
-  const size_t fixed = (size_t)DWG * 2 * C::kIPB * kXcBytes + (((size_t)p.B * p.g.kpad + 7) & ~(size_t)7) * 2 + 512;
+  const int64_t tile_bytes = (int64_t)NN * kSuperStep, sum_bytes = (int64_t)p.Bp * 8;
   int dev = 0, maxsmem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t fixed = (((size_t)p.B * p.g.kpad + 7) & ~(size_t)7) * 2 + 512;
   const int64_t avail = (int64_t)maxsmem - (int64_t)fixed - 1024;
+  // items per warpgroup per stage: fill the TMEM slot ring, but keep >= 4 stages
+  const int64_t per_item = std::max<int64_t>(p.g.ss_bytes, kWeakChunkBytes) + tile_bytes + sum_bytes;
+  static const int ipw_env = getenv("OWQ_IPW") ? atoi(getenv("OWQ_IPW")) : 0;   // experiments
+  int ipw = ipw_env > 0 ? ipw_env : C::kR;
+  while (ipw > 1 && 4 * (C::DWG * ipw * per_item + 2048) > avail) --ipw;
+  p.cap = C::DWG * ipw;
+  p.code_bytes = (int32_t)std::max<int64_t>((int64_t)p.cap * p.g.ss_bytes, (int64_t)p.cap * kWeakChunkBytes);
+  p.tile_off = p.code_bytes;
+  p.sum_off = p.tile_off + (int32_t)(p.cap * tile_bytes);
+  p.sz_off = p.sum_off + (int32_t)((p.cap * sum_bytes + 15) / 16 * 16);
+  const int sz_blocks = p.g.group ? (int)(p.cap * kSuperStep / p.g.group + 2) : 1;
+  p.stage_bytes = (p.sz_off + sz_blocks * kSZBlockBytes + 127) / 128 * 128;
   int nst = (int)(avail / (p.stage_bytes + 16));
   static const int max_nst = getenv("OWQ_NST") ? atoi(getenv("OWQ_NST")) : 8;
   nst = std::min(nst, max_nst);
   if (nst < 2) return OWQ_ERR_UNSUPPORTED;     // too many weak columns / batch rows for shared memory
   p.nst = nst;
   const size_t smem = (size_t)nst * p.stage_bytes + fixed + (size_t)nst * 16;
-  auto kern = owq_gemv_kernel<BITS, DWG, X1>;
+  auto kern = owq_gemv_kernel<BITS, NN>;
   static thread_local size_t configured = 0;
   if (configured < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -891,11 +838,22 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   kern<<<(unsigned)grid, C::kThreads, smem, stream>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    fprintf(stderr, "owq: launch of owq_gemv_kernel<%d,%d,%d> (grid %lld, smem %zu) failed: %s\n", BITS, DWG, (int)X1,
+    fprintf(stderr, "owq: launch of owq_gemv_kernel<%d,%d> (grid %lld, smem %zu) failed: %s\n", BITS, NN,
             (long long)grid, smem, cudaGetErrorString(e));
     return OWQ_ERR_CUDA;
   }
   return OWQ_OK;
+}
+
+template <int BITS>
+static owq_status launch_n(const Params& p, int64_t grid, cudaStream_t cs) {
+  switch (mma_n_for(p.B)) {
+    case 8: return launch<BITS, 8>(p, grid, cs);
+    case 16: return launch<BITS, 16>(p, grid, cs);
+    case 32: return launch<BITS, 32>(p, grid, cs);
+    case 64: return launch<BITS, 64>(p, grid, cs);
+    default: return launch<BITS, 96>(p, grid, cs);
+  }
 }
 
 static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int B, void* d_y,
@@ -913,40 +871,27 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.y = d_y;
   p.counters = (uint32_t*)d_ws;
   p.partial = (float*)((uint8_t*)d_ws + ws_counters(g));
+  uint8_t* tiles = (uint8_t*)d_ws + ws_counters(g) + ws_partials(g, B, grid);
+  long long* sums = (long long*)(tiles + ws_tiles(g, B));
+  p.tiles = tiles;
+  p.sums = sums;
   p.g = g;
   p.B = B;
+  p.Bp = batch_pad(B);
   p.y_f32 = y_f32 ? 1 : 0;
-  cudaStream_t cs = (cudaStream_t)stream;
   p.xK = g.K;
-  if ((g.K % 8) != 0 || (reinterpret_cast<uintptr_t>(d_x) & 15) != 0) {
-    // rows not 16-byte aligned for TMA: one zero-padded copy into the workspace
-    __half* xp = (__half*)((uint8_t*)d_ws + ws_counters(g) + ws_partials(g, B, grid));
-    const int Kp = g.nss * kSuperStep;
-    const int64_t n = (int64_t)B * Kp;
-    owq_pad_x_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, cs>>>(p.x, xp, B, g.K, Kp);
-    if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
-    p.x = xp;
-    p.xK = Kp;
-  }
+  cudaStream_t cs = (cudaStream_t)stream;
+  // x -> exact int8 digits in UMMA tile order, plus per-super-step digit sums
+  owq_x_digits_kernel<<<(unsigned)g.nss, 256, 0, cs>>>(p.x, p.xK, B, p.Bp, g.K, mma_n_for(B), tiles, sums);
+  if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
   static unsigned long long* trace_buf = nullptr;
   static const char* trace_path = getenv("OWQ_TRACE");
   if (trace_path && !trace_buf) cudaMalloc(&trace_buf, 4096 * 256 * 8);
   if (trace_buf) cudaMemsetAsync(trace_buf, 0, 4096 * 256 * 8, cs);
   p.trace = trace_buf;
-  static const int dbg = getenv("OWQ_DEBUG") ? atoi(getenv("OWQ_DEBUG")) : 0;
-  p.dbg = dbg;
   p.group_log2 = 0;
   if (g.group) while ((kSuperStep << p.group_log2) < g.group) ++p.group_log2;
-  static const int dwg = getenv("OWQ_DWG") ? atoi(getenv("OWQ_DWG")) : 3;
-  owq_status rs;
-  const bool x1 = B == 1;
-  if (dwg == 2) {
-    if (g.bits == 3) rs = x1 ? launch<3, 2, true>(p, grid, cs) : launch<3, 2, false>(p, grid, cs);
-    else rs = x1 ? launch<4, 2, true>(p, grid, cs) : launch<4, 2, false>(p, grid, cs);
-  } else {
-    if (g.bits == 3) rs = x1 ? launch<3, 3, true>(p, grid, cs) : launch<3, 3, false>(p, grid, cs);
-    else rs = x1 ? launch<4, 3, true>(p, grid, cs) : launch<4, 3, false>(p, grid, cs);
-  }
+  const owq_status rs = g.bits == 3 ? launch_n<3>(p, grid, cs) : launch_n<4>(p, grid, cs);
   if (trace_buf && rs == OWQ_OK) {   // experiments only: dump the per-CTA stamps
     std::vector<unsigned long long> h((size_t)grid * 256);
     cudaMemcpyAsync(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost, cs);

@@ -1,5 +1,6 @@
-// owq_layout.h -- device layout of the packed OWQ blob (layout version 2).
+// owq_layout.h -- device layout of the packed OWQ blob (layout version 3).
 // Shared by the host packer (owq_pack.cpp) and the device kernels (*.cu).
+// (Layout version 3: codes positioned for the tcgen05 kind::i8 A operand.)
 // DESIGN.md §5 documents the bit map; include/owq.h summarises it.
 //
 // Row-blocks of 128 output rows (one tcgen05 M=128 tile, one thread per row).
@@ -7,8 +8,8 @@
 //   super-step record: every row's 64 codes in WPR 32-bit words (WPR = 6 for
 //     3-bit, 8 for 4-bit); words 0..3 of row r at r*16, words 4.. at
 //     2048 + r*(WPR-4)*4 -- one LDS.128 (+ one LDS.64/128) per thread, no bank
-//     conflicts.  Pair j = columns (2j, 2j+1) of the super-step becomes TMEM
-//     column j of the thread's row (fp16x2: low half = column 2j).
+//     conflicts.  Columns 4c..4c+3 of the super-step become TMEM column c of
+//     the thread's row (4 unsigned bytes, byte 0 = column 4c).
 //   weak chunk (8 weak columns): [128 rows][8] fp16; the ragged last chunk
 //     (k % 8 columns) is [128][k % 8] fp16, unpadded.
 // Then: scale/zero blocks [nrb][G][128 rows] of (s, z) fp16 pairs, and the
@@ -144,22 +145,36 @@ OWQ_HD int64_t row_word_byte(int bits, int r, int w) {
   return w < 4 ? (int64_t)r * 16 + w * 4 : 2048 + (int64_t)r * (words_per_row(bits) - 4) * 4 + (w - 4) * 4;
 }
 
-// Location of bit `bit` of the code in pair j (columns 2j, 2j+1), half 0/1.
-//  3-bit: j < 30: word j/5, sub j%5: sub 0..2 -> field at 3*sub, sub 3..4 -> at
-//         9 + 3*(sub-3) (after >> 9 the field sits at 0 / 3); +16 for half 1.
-//         j = 30: code bit b in word b at bit 15 (+16);  j = 31: word 3+b.
-//  4-bit: word j/4, field at 4*(j%4) (+16).
-OWQ_HD void code_bit_loc(int bits, int j, int half, int bit, int& word, int& pos) {
+// Location of bit `bit` of the code of super-step column `col` (0..63).  The
+// decoder emits 16 32-bit values per row, value c = the codes of columns
+// 4c .. 4c+3 as bytes 0..3 (tcgen05 kind::i8 A operand, one TMEM column); byte
+// b = col % 4 of value c = col / 4 sits in bits [8b, 8b+8) of a word:
+//  4-bit: c < 8 -> word c, bits 8b+0..3;  c >= 8 -> word c-8, bits 8b+4..7.
+//  3-bit: c < 6 -> word c, bits 8b+0..2;  6 <= c < 12 -> word c-6, bits 8b+3..5;
+//         c = 12+r -> bits 0,1 in word r at 8b+6, 8b+7 and bit 2 in word
+//         4 + r/2 at 8b + 6 + r%2.
+// So value c costs one LOP3 (c < 6 / c < 8), one SHF + LOP3 (c < 12 / c >= 8),
+// or two SHF + three LOP3 (3-bit c >= 12).
+OWQ_HD void code_bit_loc(int bits, int col, int bit, int& word, int& pos) {
+  const int c = col >> 2, b = col & 3;
   if (bits == 4) {
-    word = j >> 2;
-    pos = 4 * (j & 3) + bit + 16 * half;
-  } else if (j < 30) {
-    word = j / 5;
-    const int sub = j % 5;
-    pos = (sub < 3 ? 3 * sub : 9 + 3 * (sub - 3)) + bit + 16 * half;
+    word = c & 7;
+    pos = 8 * b + (c >= 8 ? 4 : 0) + bit;
+  } else if (c < 6) {
+    word = c;
+    pos = 8 * b + bit;
+  } else if (c < 12) {
+    word = c - 6;
+    pos = 8 * b + 3 + bit;
   } else {
-    word = (j - 30) * 3 + bit;
-    pos = 15 + 16 * half;
+    const int r = c - 12;
+    if (bit < 2) {
+      word = r;
+      pos = 8 * b + 6 + bit;
+    } else {
+      word = 4 + (r >> 1);
+      pos = 8 * b + 6 + (r & 1);
+    }
   }
 }
 

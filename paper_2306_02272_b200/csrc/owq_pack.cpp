@@ -139,17 +139,16 @@ void write_blob(const Layer& L, uint8_t* blob) {
         const int row = rb * owq::kRowBlock + rr;
         uint32_t words[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (row < L.M) {
-          for (int j = 0; j < owq::kSuperStep / 2; ++j)
-            for (int half = 0; half < 2; ++half) {
-              const int col = ss * owq::kSuperStep + 2 * j + half;
-              const uint32_t code = col < L.K ? L.codes[(size_t)row * L.K + col] : 0u;
-              for (int bit = 0; bit < L.bits; ++bit) {
-                if (!((code >> bit) & 1u)) continue;
-                int word, pos;
-                owq::code_bit_loc(L.bits, j, half, bit, word, pos);
-                words[word] |= 1u << pos;
-              }
+          for (int cc = 0; cc < owq::kSuperStep; ++cc) {
+            const int col = ss * owq::kSuperStep + cc;
+            const uint32_t code = col < L.K ? L.codes[(size_t)row * L.K + col] : 0u;
+            for (int bit = 0; bit < L.bits; ++bit) {
+              if (!((code >> bit) & 1u)) continue;
+              int word, pos;
+              owq::code_bit_loc(L.bits, cc, bit, word, pos);
+              words[word] |= 1u << pos;
             }
+          }
         }
         for (int w = 0; w < wpr; ++w) std::memcpy(ssrec + owq::row_word_byte(L.bits, rr, w), &words[w], 4);
       }
@@ -305,18 +304,17 @@ owq_status owq_blob_decode_host(const void* h_blob, size_t bytes, owq_shape* sha
           uint32_t words[8];
           for (int w = 0; w < wpr; ++w)
             std::memcpy(&words[w], rec + (int64_t)ss * g.ss_bytes + owq::row_word_byte(h.bits, rr, w), 4);
-          for (int j = 0; j < owq::kSuperStep / 2; ++j)
-            for (int half = 0; half < 2; ++half) {
-              const int col = ss * owq::kSuperStep + 2 * j + half;
-              if (col >= h.K) continue;
-              uint32_t c = 0;
-              for (int bit = 0; bit < h.bits; ++bit) {
-                int word, pos;
-                owq::code_bit_loc(h.bits, j, half, bit, word, pos);
-                c |= ((words[word] >> pos) & 1u) << bit;
-              }
-              codes[(size_t)row * h.K + col] = (uint8_t)c;
+          for (int cc = 0; cc < owq::kSuperStep; ++cc) {
+            const int col = ss * owq::kSuperStep + cc;
+            if (col >= h.K) continue;
+            uint32_t c = 0;
+            for (int bit = 0; bit < h.bits; ++bit) {
+              int word, pos;
+              owq::code_bit_loc(h.bits, cc, bit, word, pos);
+              c |= ((words[word] >> pos) & 1u) << bit;
             }
+            codes[(size_t)row * h.K + col] = (uint8_t)c;
+          }
         }
       }
       if (weak_val) {

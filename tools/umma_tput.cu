@@ -71,9 +71,9 @@ int main() {
   unsigned long long* d;
   cudaMalloc(&d, 8);
   const int iters = 4096;
-  run<16, true, 1, 1>(d, iters); run<16, true, 1, 2>(d, iters); run<16, true, 1, 4>(d, iters);
-  run<16, false, 1, 2>(d, iters); run<16, false, 1, 4>(d, iters);
-  run<16, true, 1, 1, 64>(d, iters); run<16, true, 1, 2, 64>(d, iters); run<8, true, 1, 1, 64>(d, iters);
-  run<32, true, 1, 2>(d, iters);
+  run<16, true, 1, 1>(d, iters); run<16, true, 2, 1>(d, iters); run<16, true, 4, 1>(d, iters); run<16, true, 8, 1>(d, iters);
+  run<16, true, 4, 2>(d, iters); run<16, true, 4, 3>(d, iters); run<16, true, 4, 4>(d, iters);
+  run<16, false, 4, 1>(d, iters); run<16, false, 8, 1>(d, iters);
+  run<32, true, 4, 1>(d, iters); run<64, true, 4, 1>(d, iters);
   return 0;
 }
