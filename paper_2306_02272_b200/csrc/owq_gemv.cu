@@ -92,20 +92,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, 0x989680;\n\t"   // suspend-time hint: sleep, don't spin
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
       "@!P bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
-}
-// wait with cycle accounting into a shared counter (trace/experiment mode only)
-__device__ __forceinline__ void mbar_wait_p(uint64_t* bar, uint32_t parity, unsigned long long* acc) {
-  if (acc) {
-    const long long t0 = clock64();
-    mbar_wait(bar, parity);
-    if ((threadIdx.x & 31) == 0) atomicAdd(acc, (unsigned long long)(clock64() - t0));
-  } else {
-    mbar_wait(bar, parity);
-  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
   asm volatile(
@@ -216,60 +206,50 @@ __device__ __forceinline__ void decode_row(const uint32_t* w, uint32_t* o) {
   }
 }
 
-// ---- x -> int8 digits (one CTA per super-step) -----------------------------------
+// ---- x -> int8 digits (one CTA per super-step, one thread per (batch row, column))
 // x * 2^24 = sum_{i<6} d_i 256^i with d_i in [-128, 127] (balanced base 256).
-__device__ __forceinline__ long long x_fixed(__half h) { return (long long)(__half2float(h) * 16777216.0f); }
-__device__ __forceinline__ int x_digit(long long X, int i) {
-  for (int j = 0; j < i; ++j) {
-    const int d = (int)(signed char)(X & 0xFF);
-    X = (X - d) >> 8;
-  }
-  return (int)(signed char)(X & 0xFF);
-}
 // tiles: [nss][NN*64] bytes; byte ((kc * NN/8 + nb) * 8 + r) * 16 + kk holds digit
-// row n = 8 nb + r (= 6 b + i), column k = 16 kc + kk of the super-step.
+// row n = 8 nb + r (= 6 b + i; rows >= 6 B are zero), column k = 16 kc + kk of the
+// super-step.  sums: [nss][Bp] = sum over the super-step's columns of x * 2^24.
+__device__ __forceinline__ long long x_fixed(__half h) { return (long long)(__half2float(h) * 16777216.0f); }
 __global__ void owq_x_digits_kernel(const __half* __restrict__ x, int64_t xK, int B, int Bp, int K, int NN,
                                     uint8_t* __restrict__ tiles, long long* __restrict__ sums) {
+  __shared__ long long part[2 * OWQ_MAX_BATCH];
   const int ss = blockIdx.x;
+  const int b = threadIdx.x >> 6, k = threadIdx.x & 63;   // blockDim = 64 * Bp
   const int nbk = NN / 8;
-  uint32_t* tile = reinterpret_cast<uint32_t*>(tiles + (int64_t)ss * NN * 64);
-  for (int p4 = threadIdx.x; p4 < NN * 16; p4 += blockDim.x) {
-    uint32_t word = 0;
+  const int64_t col = (int64_t)ss * kSuperStep + k;
+  long long X = (b < B && col < K) ? x_fixed(x[(int64_t)b * xK + col]) : 0;
+  uint8_t* tile = tiles + (int64_t)ss * NN * 64 + (k >> 4) * nbk * 128 + (k & 15);
+  if (b < B) {
+    long long t = X;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int pos = p4 * 4 + t;
-      const int kk = pos & 15, r = (pos >> 4) & 7, blk = pos >> 7;
-      const int nb = blk % nbk, kc = blk / nbk;
-      const int n = nb * 8 + r;
-      const int64_t col = (int64_t)ss * kSuperStep + kc * 16 + kk;
-      int d = 0;
-      if (n < kDigits * B && col < K) d = x_digit(x_fixed(x[(int64_t)(n / kDigits) * xK + col]), n % kDigits);
-      word |= (uint32_t)(uint8_t)d << (8 * t);
+    for (int i = 0; i < kDigits; ++i) {
+      const int d = (int)(signed char)(t & 0xFF);
+      t = (t - d) >> 8;
+      const int n = kDigits * b + i;
+      tile[(n >> 3) * 128 + (n & 7) * 16] = (uint8_t)d;
     }
-    tile[p4] = word;
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int b = warp; b < Bp; b += blockDim.x >> 5) {
-    long long s = 0;
-    if (b < B)
-      for (int k = lane; k < kSuperStep; k += 32) {
-        const int64_t col = (int64_t)ss * kSuperStep + k;
-        if (col < K) s += x_fixed(x[(int64_t)b * xK + col]);
-      }
+  if (b == 0)   // zero the padding rows 6B .. NN-1 of this column
+    for (int n = kDigits * B; n < NN; ++n) tile[(n >> 3) * 128 + (n & 7) * 16] = 0;
+  long long v = X;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) sums[(int64_t)ss * Bp + b] = s;
-  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (k == 0) sums[(int64_t)ss * Bp + b] = part[2 * b] + part[2 * b + 1];
 }
 
 // group of code item li (row-block relative super-step index)
 __device__ __forceinline__ int group_of(const Params& p, int li) { return p.g.group ? (li >> p.group_log2) : 0; }
 
-// Per MMA-N class: decode warpgroups, TMEM A slots per warpgroup, largest batch.
+// Per MMA-N class: decode warpgroups, items per warpgroup per stage, largest batch.
+// Each warpgroup owns two TMEM A buffers (ping-pong) of kIPW items.
 template <int BITS, int NN>
 struct Cfg {
   static constexpr int DWG = NN <= 32 ? 4 : 2;
-  static constexpr int kR = NN <= 32 ? 4 : (NN == 64 ? 8 : 4);
+  static constexpr int kIPW = NN <= 16 ? 3 : NN == 32 ? 2 : NN == 64 ? 4 : 2;
   static constexpr int kMaxB = NN == 8 ? 1 : NN == 16 ? 2 : NN == 32 ? 5 : NN == 64 ? 10 : 16;
   static constexpr int kDecodeWarps = 4 * DWG;            // DWG decode warpgroups
   static constexpr int kEpiWarp0 = kDecodeWarps;          // 4 epilogue warps (warp % 4 = TMEM lane quarter)
@@ -279,7 +259,8 @@ struct Cfg {
   static constexpr int kThreads = kWarps * 32;
   static constexpr int kTmemCols = 512;
   static constexpr int kACols = kSuperStep / 4;           // 16 TMEM columns (4 code bytes each) per item
-  static constexpr int kDCol0 = DWG * kR * kACols;        // then D: [DWG][2] x NN columns
+  static constexpr int kABuf = kIPW * kACols;            // TMEM columns per A buffer
+  static constexpr int kDCol0 = DWG * 2 * kABuf;          // A: [DWG][2] buffers, then D: [DWG][2] x NN columns
   static_assert(kDCol0 + DWG * 2 * NN <= kTmemCols, "TMEM budget");
   static_assert(kMaxB * kDigits <= NN, "digit rows");
   // per stage: decode + epilogue warps arrive, each MMA warp commits (B is read from the stage)
@@ -320,7 +301,7 @@ __device__ __forceinline__ void share(int n, int w, int dwg, int& lo, int& hi) {
 template <int BITS, int NN>
 __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(const Params p) {
   using C = Cfg<BITS, NN>;
-  constexpr int DWG = C::DWG, R = C::kR, MAXB = C::kMaxB;
+  constexpr int DWG = C::DWG, MAXB = C::kMaxB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geo& g = p.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -330,28 +311,25 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
   uint64_t* bars = reinterpret_cast<uint64_t*>(xw + (((size_t)p.B * g.kpad + 7) & ~(size_t)7));
   uint64_t* full = bars;
   uint64_t* empty = full + NST;
-  uint64_t* afull = empty + NST;       // [DWG][R]  A item slot written (4 warps)
-  uint64_t* aempty = afull + DWG * R;  // [DWG][R]  MMA done reading it
-  uint64_t* dfull = aempty + DWG * R;  // [DWG][2]  group accumulator complete
+  uint64_t* afull = empty + NST;       // [DWG][2]  A buffer written (4 warps)
+  uint64_t* aempty = afull + DWG * 2;  // [DWG][2]  MMA done reading it
+  uint64_t* dfull = aempty + DWG * 2;  // [DWG][2]  group accumulator complete
   uint64_t* dempty = dfull + 2 * DWG;  // [DWG][2]  epilogue drained it
-  unsigned long long* wprof = reinterpret_cast<unsigned long long*>(dempty + 2 * DWG);   // [8] wait cycles
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wprof + 8);
+  int64_t* span = reinterpret_cast<int64_t*>(dempty + 2 * DWG);   // [2] this CTA's item range
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(span + 2);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
-  // wait accounting slots (OWQ_TRACE): 0 decode/full 1 decode/aempty 2 mma/afull
-  // 3 mma/dempty 4 epi/full 5 epi/dfull 6 prod/empty
-  unsigned long long* const WP = p.trace ? wprof : nullptr;
 
   const int64_t grid = gridDim.x, cta = blockIdx.x;
-  // the host caps the grid so that every CTA's byte window holds an item start
-  const int64_t i0 = cta_first_item(g, grid, cta), i1 = cta_first_item(g, grid, cta + 1);
-  if (p.trace && threadIdx.x == 0) p.trace[cta * 256 + 0] = gtime();
-
   if (threadIdx.x == 0) {
+    if (p.trace) p.trace[cta * 256 + 0] = gtime();
+    // the host caps the grid so that every CTA's byte window holds an item start
+    span[0] = cta_first_item(g, grid, cta);
+    span[1] = cta_first_item(g, grid, cta + 1);
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); }
-    for (int i = 0; i < DWG * R; ++i) { mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); }
-    for (int i = 0; i < 2 * DWG; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
+    for (int i = 0; i < 2 * DWG; ++i) {
+      mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int i = 0; i < 8; ++i) wprof[i] = 0ull;
   }
   if (warp == C::kProdWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
@@ -362,6 +340,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int64_t i0 = span[0], i1 = span[1];
   const int n_rb = items_per_rb(g);
   const uint32_t tile_bytes = (uint32_t)NN * kSuperStep;
   const uint32_t sum_bytes = (uint32_t)p.Bp * 8u;
@@ -377,7 +356,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
       int s = 0, k = 0;
       uint32_t ph = 0;
       while ((n = it.next(srb, sli)) > 0) {
-        if (k >= NST) mbar_wait_p(&empty[s], ph ^ 1u, WP ? WP + 6 : nullptr);
+        if (k >= NST) mbar_wait(&empty[s], ph ^ 1u);
         if (p.trace && k < 32) p.trace[cta * 256 + 64 + k] = gtime();
         uint8_t* st = ring + (size_t)s * p.stage_bytes;
         const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
@@ -400,15 +379,15 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
     }
   } else if (warp < C::kDecodeWarps) {
     // ==================================================================== decode
-    // Warpgroup wg decodes a contiguous share of every code stage, one item
-    // (128 rows x 64 codes) into one TMEM slot of its R-slot ring, and publishes
-    // each item to its MMA warp (afull); the slot comes back through aempty.
+    // Warpgroup wg decodes a contiguous share (<= kIPW items of 128 rows x 64
+    // codes) of every code stage into one of its two TMEM A buffers and
+    // publishes the buffer to its MMA warp (afull); it comes back via aempty.
     const int wg = warp >> 2, q = warp & 3;
     const int row = q * 32 + lane;                      // TMEM lane / row inside the row-block
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * R * C::kACols);
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * 2 * C::kABuf);
     const uint32_t ss = (uint32_t)g.ss_bytes;
     constexpr uint32_t kHiStride = BITS == 3 ? 8u : 16u;   // words 4.. of a row
-    uint32_t slot = 0, rnd = 0;                         // ring position, completed rounds
+    uint32_t acnt = 0;                                  // A buffers published
     StageIter it;
     it.init(g, i0, i1, p.cap);
     int64_t srb;
@@ -417,15 +396,21 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
     uint32_t ph = 0;
     int kst = 0;
     while ((n = it.next(srb, sli)) > 0) {
-      mbar_wait_p(&full[s], ph, WP ? WP + 0 : nullptr);
+      mbar_wait(&full[s], ph);
       if (p.trace && warp == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 192 + kst] = gtime();
-      if (sli < g.nss) {
+      int lo, hi;
+      share(n, wg, DWG, lo, hi);
+      if (sli < g.nss && lo < hi) {
+        const uint32_t buf = acnt & 1u;
+        if (acnt >= 2) mbar_wait(&aempty[wg * 2 + buf], ((acnt >> 1) & 1u) ^ 1u);
+        if (p.trace && warp == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 18 + kst] = gtime();
+        ++acnt;
+        tc_fence_after();
         const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
-        int lo, hi;
-        share(n, wg, DWG, lo, hi);
         uint32_t a_lo = sbase + (uint32_t)lo * ss + (uint32_t)row * 16u;
         uint32_t a_hi = sbase + (uint32_t)lo * ss + 2048u + (uint32_t)row * kHiStride;
-        for (int pi = lo; pi < hi; ++pi, a_lo += ss, a_hi += ss) {
+        uint32_t tcol = trow + buf * (uint32_t)C::kABuf;
+        for (int pi = lo; pi < hi; ++pi, a_lo += ss, a_hi += ss, tcol += C::kACols) {
           uint32_t w[8];
           {
             const uint4 a = lds128(a_lo);
@@ -440,15 +425,12 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
           }
           uint32_t o[16];
           decode_row<BITS>(w, o);
-          if (rnd) mbar_wait_p(&aempty[wg * R + slot], (rnd - 1u) & 1u, WP ? WP + 1 : nullptr);
-          tc_fence_after();
-          tc_st16(trow + slot * (uint32_t)C::kACols, o);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&afull[wg * R + slot]);
-          if (++slot == (uint32_t)R) { slot = 0; ++rnd; }
+          tc_st16(tcol, o);
         }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[wg * 2 + buf]);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -460,9 +442,9 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
     // ==================================================================== MMA issue (one warp per warpgroup)
     const int wg = warp - C::kMmaWarp0;
     if (lane == 0) {
-      uint32_t slot = 0, rnd = 0, dcnt = 0;
+      uint32_t acnt = 0, dcnt = 0;
       bool open = false;          // D[dcnt & 1] holds a partial group sum
-      const uint32_t a_wg = tmem + (uint32_t)(wg * R * C::kACols);
+      const uint32_t a_wg = tmem + (uint32_t)(wg * 2 * C::kABuf);
       constexpr uint32_t kLbo = (NN / 8) * 128;        // K-adjacent core matrices
       StageIter it;
       it.init(g, i0, i1, p.cap);
@@ -476,15 +458,21 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
           const uint32_t stile = smem_addr(ring + (size_t)s * p.stage_bytes) + (uint32_t)p.tile_off;
           int lo, hi;
           share(cn, wg, DWG, lo, hi);
+          uint32_t buf = 0;
+          if (lo < hi) {
+            buf = acnt & 1u;
+            mbar_wait(&afull[wg * 2 + buf], (acnt >> 1) & 1u);
+            if (p.trace && wg == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
+            ++acnt;
+            tc_fence_after();
+          }
           for (int pa = 0; pa < cn;) {
             const Seg sg = segment(p, pa, cn, cli, crb, nn, nrb, nli);
             const int a0 = sg.pa > lo ? sg.pa : lo, a1 = sg.pb + 1 < hi ? sg.pb + 1 : hi;
             for (int pi = a0; pi < a1; ++pi) {
-              mbar_wait_p(&afull[wg * R + slot], rnd & 1u, WP ? WP + 2 : nullptr);
-              tc_fence_after();
               const uint32_t dbuf = dcnt & 1u;
-              if (!open && dcnt >= 2) mbar_wait_p(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u, WP ? WP + 3 : nullptr);
-              const uint32_t a_t = a_wg + slot * (uint32_t)C::kACols;
+              if (!open && dcnt >= 2) mbar_wait(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
+              const uint32_t a_t = a_wg + buf * (uint32_t)C::kABuf + (uint32_t)(pi - lo) * C::kACols;
               const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * NN);
               const uint32_t tb = stile + (uint32_t)pi * tile_bytes;
 #pragma unroll
@@ -492,8 +480,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
                 tc_mma_i8(d_t, a_t + 8 * j, umma_desc(tb + j * 2 * kLbo, kLbo, 128), idesc_i8<NN>(),
                           (open || j > 0) ? 1u : 0u);
               open = true;
-              tc_commit(&aempty[wg * R + slot]);   // slot consumed once these MMAs complete
-              if (++slot == (uint32_t)R) { slot = 0; ++rnd; }
             }
             if (sg.ends && open) {
               tc_commit(&dfull[wg * 2 + (dcnt & 1u)]);
@@ -502,6 +488,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
             }
             pa = sg.pb + 1;
           }
+          if (lo < hi) tc_commit(&aempty[wg * 2 + buf]);   // buffer consumed once these MMAs complete
         }
         tc_commit(&empty[s]);   // the stage's digit tiles are free once these MMAs completed
         if (p.trace && wg == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
@@ -544,7 +531,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
     uint32_t ph = 0;
     while (cn > 0) {
       const int32_t nn = it.next(nrb, nli);
-      mbar_wait_p(&full[s], ph, WP ? WP + 4 : nullptr);
+      mbar_wait(&full[s], ph);
       const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
       if (cli < g.nss) {
         const int gi0 = group_of(p, cli);
@@ -576,7 +563,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
             for (int w = 0; w < DWG; ++w) {
               if (part & (1u << w)) {   // fixed order over warpgroups: deterministic
                 const uint32_t dbuf = dcnt[w] & 1u;
-                mbar_wait_p(&dfull[w * 2 + dbuf], (dcnt[w] >> 1) & 1u, WP ? WP + 5 : nullptr);
+                mbar_wait(&dfull[w * 2 + dbuf], (dcnt[w] >> 1) & 1u);
                 tc_fence_after();
                 const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * NN);
 #pragma unroll
@@ -706,10 +693,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
   }
-  if (p.trace && threadIdx.x == 0) {
-    p.trace[cta * 256 + 62] = gtime();
-    for (int i = 0; i < 8; ++i) p.trace[cta * 256 + 10 + i] = wprof[i];
-  }
+  if (p.trace && threadIdx.x == 0) p.trace[cta * 256 + 62] = gtime();
 }
 
 // Device inverse of the code layout (test hook): one CTA (128 threads = rows) per
@@ -813,7 +797,7 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   // items per warpgroup per stage: fill the TMEM slot ring, but keep >= 4 stages
   const int64_t per_item = std::max<int64_t>(p.g.ss_bytes, kWeakChunkBytes) + tile_bytes + sum_bytes;
   static const int ipw_env = getenv("OWQ_IPW") ? atoi(getenv("OWQ_IPW")) : 0;   // experiments
-  int ipw = ipw_env > 0 ? ipw_env : C::kR;
+  int ipw = ipw_env > 0 && ipw_env < C::kIPW ? ipw_env : C::kIPW;
   while (ipw > 1 && 4 * (C::DWG * ipw * per_item + 2048) > avail) --ipw;
   p.cap = C::DWG * ipw;
   p.code_bytes = (int32_t)std::max<int64_t>((int64_t)p.cap * p.g.ss_bytes, (int64_t)p.cap * kWeakChunkBytes);
@@ -882,7 +866,7 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.xK = g.K;
   cudaStream_t cs = (cudaStream_t)stream;
   // x -> exact int8 digits in UMMA tile order, plus per-super-step digit sums
-  owq_x_digits_kernel<<<(unsigned)g.nss, 256, 0, cs>>>(p.x, p.xK, B, p.Bp, g.K, mma_n_for(B), tiles, sums);
+  owq_x_digits_kernel<<<(unsigned)g.nss, 64 * p.Bp, 0, cs>>>(p.x, p.xK, B, p.Bp, g.K, mma_n_for(B), tiles, sums);
   if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
   static unsigned long long* trace_buf = nullptr;
   static const char* trace_path = getenv("OWQ_TRACE");

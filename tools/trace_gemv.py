@@ -20,15 +20,11 @@ t0 = t[:, 0].min()
 def rel(v): return (v - t0) / 1e3
 print(f"{M}x{K} b{bits} CTAs={len(t)}  (us from first CTA start; median over CTAs)")
 print(f" start med {np.median(rel(t[:,0])):.2f}  fin-in {np.median(rel(t[:,50])):.2f}  fin-out {np.median(rel(t[:,56])):.2f}  end {np.median(rel(t[:,62])):.2f} max {rel(t[:,62]).max():.2f}")
-print(" stage  prod_issue  dec_full  dec_done  mma_done  epi_done")
+print(" stage  prod_issue  dec_full dec_aempty  dec_done mma_afull  mma_done  epi_done")
 for kk in range(0, 16):
-    cols = [64 + kk, 192 + kk, 96 + kk, 128 + kk, 160 + kk]
+    cols = [64 + kk, 192 + kk, 18 + kk, 96 + kk, 224 + kk, 128 + kk, 160 + kk]
     vals = []
     for c in cols:
         v = t[:, c]; v = v[v > 0]
         vals.append(f"{np.median(rel(v)):9.2f}" if len(v) else "        -")
     print(f" {kk:5d} " + " ".join(vals))
-names = ["decode/full", "decode/aempty", "mma/afull", "mma/dempty", "epi/full", "epi/dfull", "prod/empty"]
-print(" wait cycles per CTA (sum over waiting warps' lane 0), mean:")
-for i, nme in enumerate(names):
-    print(f"   {nme:14s} {t[:, 10 + i].mean():12.0f}")
