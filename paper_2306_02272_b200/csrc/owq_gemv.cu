@@ -49,7 +49,8 @@ constexpr int kDigits = 6;          // int8 digits per x value (base 256, balanc
 
 // MMA N (digit rows of B) for a batch: 6 * B padded to a valid tcgen05 N
 static inline int mma_n_for(int B) {
-  const int r = kDigits * B;
+  static const int min_n = getenv("OWQ_MINN") ? atoi(getenv("OWQ_MINN")) : 8;   // experiments
+  const int r = std::max(kDigits * B, min_n);
   return r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 96;
 }
 static inline int batch_pad(int B) { return (B + 1) & ~1; }   // digit-sum rows (16-byte aligned runs)
@@ -69,12 +70,11 @@ struct Params {
   int32_t cap;            // items per stage
   int32_t code_bytes;     // stage region for codes / weak chunks
   int32_t tile_off;       // digit tiles inside a stage
-  int32_t sum_off;        // digit sums inside a stage
-  int32_t sz_off;         // scale/zero blocks inside a stage
   int32_t stage_bytes;
   int64_t xK;             // row stride of x in elements
   int32_t group_log2;     // log2(group_size / 64)
   unsigned long long* trace;   // experiments only (OWQ_TRACE)
+  int32_t exp;                 // experiments only (OWQ_EXP): 3 = skip the TMEM stores
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -150,6 +150,51 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
                : "memory");
 }
+// Warp-uniform forms: the whole warp executes them, one elected lane issues.
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8_elect(uint32_t d_t, uint32_t a_t, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_t),
+      "r"(a_t), "l"(b_desc), "r"(idesc), "r"(acc));
+}
+// All 2*IPW MMAs of a full warpgroup share of a stage under ONE elect: item t,
+// half j reads TMEM A columns a0 + 16t + 8j and the digit tile at
+// b0 + t*TILE + j*2*LBO bytes (descriptor start field = address >> 4).
+template <int IPW, uint32_t TILE, uint32_t LBO>
+__device__ __forceinline__ void tc_mma_i8_stage(uint32_t d_t, uint32_t a0, uint64_t b0, uint32_t idesc, uint32_t acc) {
+#define OWQ_MMA_T(t)                                                                              \
+  "add.u32 a, %1, " #t "*16;\n\t"                                                                  \
+  "add.u64 b, %2, " #t "*(%5/16);\n\t"                                                             \
+  "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a], b, %3, p;\n\t"                                  \
+  "setp.eq.u32 p, 0, 0;\n\t"                                                                      \
+  "add.u32 a, a, 8;\n\t"                                                                           \
+  "add.u64 b, b, %6/16;\n\t"                                                                       \
+  "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a], b, %3, p;\n\t"
+  static_assert(IPW >= 1 && IPW <= 4, "IPW");
+  if (IPW == 1)
+    asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) "}" ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc), "r"(acc),
+                 "n"(TILE), "n"(2 * LBO));
+  else if (IPW == 2)
+    asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) "}" ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc),
+                 "r"(acc), "n"(TILE), "n"(2 * LBO));
+  else if (IPW == 3)
+    asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) "}" ::"r"(d_t), "r"(a0), "l"(b0),
+                 "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
+  else
+    asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) OWQ_MMA_T(3) "}" ::"r"(d_t),
+                 "r"(a0), "l"(b0), "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
+#undef OWQ_MMA_T
+}
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_t, uint32_t a_t, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -185,24 +230,38 @@ __host__ __device__ constexpr uint32_t idesc_i8() {
 }
 
 // Codes of one row's super-step -> 16 words, word c = codes of columns 4c..4c+3
-// as bytes (the bit map of owq_layout.h::code_bit_loc).
+// as bytes (the bit map of owq_layout.h::code_bit_loc).  The ALU pipe (LOP3,
+// SHF: half rate) is this kernel's binding resource, so the right shifts run on
+// the otherwise idle FMA pipe as IMAD.HI: w >> k = umulhi(w, 2^(32-k)), with
+// the multipliers held in registers (opaque to the compiler, which would turn a
+// literal power of two back into SHF).
+struct Shifts { uint32_t m3, m4, m5, m6; };
+__device__ __forceinline__ Shifts make_shifts() {
+  Shifts h;
+  asm volatile("mov.b32 %0, %1;" : "=r"(h.m3) : "n"(1u << 29));
+  asm volatile("mov.b32 %0, %1;" : "=r"(h.m4) : "n"(1u << 28));
+  asm volatile("mov.b32 %0, %1;" : "=r"(h.m5) : "n"(1u << 27));
+  asm volatile("mov.b32 %0, %1;" : "=r"(h.m6) : "n"(1u << 26));
+  return h;
+}
 template <int BITS>
-__device__ __forceinline__ void decode_row(const uint32_t* w, uint32_t* o) {
+__device__ __forceinline__ void decode_row(const uint32_t* w, uint32_t* o, const Shifts& h) {
   if (BITS == 4) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       o[i] = w[i] & 0x0F0F0F0Fu;
-      o[8 + i] = (w[i] >> 4) & 0x0F0F0F0Fu;
+      o[8 + i] = __umulhi(w[i], h.m4) & 0x0F0F0F0Fu;
     }
   } else {
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
       o[i] = w[i] & 0x07070707u;
-      o[6 + i] = (w[i] >> 3) & 0x07070707u;
+      o[6 + i] = __umulhi(w[i], h.m3) & 0x07070707u;
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r)
-      o[12 + r] = ((w[r] >> 6) & 0x03030303u) | ((w[4 + (r >> 1)] >> (4 + (r & 1))) & 0x04040404u);
+      o[12 + r] = (__umulhi(w[r], h.m6) & 0x03030303u) |
+                  (__umulhi(w[4 + (r >> 1)], (r & 1) ? h.m5 : h.m4) & 0x04040404u);
   }
 }
 
@@ -267,35 +326,54 @@ struct Cfg {
   static constexpr int kEmptyCount = kDecodeWarps + 4 + DWG;
 };
 
+// Stage descriptor, written by the producer into shared memory before it
+// arms the stage's full barrier (consumers read it after the wait: the
+// mbarrier arrive/wait pair orders it).  n == 0 terminates the consumers.
+struct StageDesc {
+  int32_t rb;        // row-block
+  int16_t li;        // first item (row-block relative)
+  uint8_t n;         // items
+  uint8_t flags;     // kRbEnd: last stage of this row-block in the CTA;
+                     // kGroupCont: the stage's last scale group continues in the next stage
+};
+constexpr uint8_t kRbEnd = 1, kGroupCont = 2;
+
 // Segments of a code stage: maximal runs of items of one scale group.  For
 // per-row scales a stage is one segment.  `ends` = the segment's group has no
-// further item in this CTA's sequence (the next item is in another group or
-// row-block, a weak chunk, or absent).
+// further item in this CTA's sequence.
 struct Seg {
   int pa, pb, gi;
   bool ends;
 };
-__device__ __forceinline__ Seg segment(const Params& p, int pa, int cn, int cli, int64_t crb, int nn, int64_t nrb,
-                                       int nli) {
+__device__ __forceinline__ Seg segment(const Params& p, int pa, const StageDesc& d) {
   Seg sg;
   sg.pa = pa;
-  sg.gi = group_of(p, cli + pa);
+  sg.gi = group_of(p, d.li + pa);
   if (p.g.group) {
-    const int gend = ((sg.gi + 1) << p.group_log2) - cli - 1;   // last stage position of this group
-    sg.pb = gend < cn - 1 ? gend : cn - 1;
+    const int gend = ((sg.gi + 1) << p.group_log2) - d.li - 1;   // last stage position of this group
+    sg.pb = gend < d.n - 1 ? gend : d.n - 1;
   } else {
-    sg.pb = cn - 1;
+    sg.pb = d.n - 1;
   }
-  if (sg.pb + 1 < cn) sg.ends = true;
-  else sg.ends = !(nn > 0 && nrb == crb && nli < p.g.nss && group_of(p, nli) == sg.gi);
+  sg.ends = sg.pb + 1 < d.n || !(d.flags & kGroupCont);
   return sg;
 }
 // contiguous share of a stage's n items owned by warpgroup w: [lo, hi)
-__device__ __forceinline__ void share(int n, int w, int dwg, int& lo, int& hi) {
-  const int per = (n + dwg - 1) / dwg;
+template <int DWG>
+__device__ __forceinline__ void share(int n, int w, int& lo, int& hi) {
+  const int per = (n + DWG - 1) / DWG;
   lo = w * per;
   hi = lo + per < n ? lo + per : n;
   if (lo > n) lo = n;
+}
+__device__ __forceinline__ StageDesc load_desc(const StageDesc* d) {
+  const uint2 v = lds64(smem_addr(d));
+  StageDesc r;
+  r.rb = (int32_t)v.x;
+  r.li = (int16_t)(v.y & 0xFFFF);
+  r.n = (uint8_t)((v.y >> 16) & 0xFF);
+  r.flags = (uint8_t)(v.y >> 24);
+  return r;
 }
 
 template <int BITS, int NN>
@@ -308,14 +386,17 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
   const int NST = p.nst;
   uint8_t* ring = smem;
   __half* xw = reinterpret_cast<__half*>(smem + (size_t)NST * p.stage_bytes);   // [B][kpad] x at the weak columns
-  uint64_t* bars = reinterpret_cast<uint64_t*>(xw + (((size_t)p.B * g.kpad + 7) & ~(size_t)7));
+  long long* red = reinterpret_cast<long long*>(xw + (((size_t)p.B * g.kpad + 7) & ~(size_t)7));   // [2][4][16]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(red + 2 * 4 * OWQ_MAX_BATCH);
   uint64_t* full = bars;
   uint64_t* empty = full + NST;
   uint64_t* afull = empty + NST;       // [DWG][2]  A buffer written (4 warps)
   uint64_t* aempty = afull + DWG * 2;  // [DWG][2]  MMA done reading it
   uint64_t* dfull = aempty + DWG * 2;  // [DWG][2]  group accumulator complete
   uint64_t* dempty = dfull + 2 * DWG;  // [DWG][2]  epilogue drained it
-  int64_t* span = reinterpret_cast<int64_t*>(dempty + 2 * DWG);   // [2] this CTA's item range
+  StageDesc* desc = reinterpret_cast<StageDesc*>(dempty + 2 * DWG);   // [NST]
+  uint4* mbox = reinterpret_cast<uint4*>(desc + NST + (NST & 1));     // [DWG][2] decode -> MMA stage notes
+  int64_t* span = reinterpret_cast<int64_t*>(mbox + 2 * DWG);         // [2] this CTA's item range
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(span + 2);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
 
@@ -343,7 +424,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
   const int64_t i0 = span[0], i1 = span[1];
   const int n_rb = items_per_rb(g);
   const uint32_t tile_bytes = (uint32_t)NN * kSuperStep;
-  const uint32_t sum_bytes = (uint32_t)p.Bp * 8u;
 
   if (warp == C::kProdWarp) {
     // ==================================================================== producer
@@ -351,153 +431,203 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
       const uint64_t pol = evict_first_policy(), pol_x = evict_last_policy();
       StageIter it;
       it.init(g, i0, i1, p.cap);
-      int64_t srb;
-      int32_t sli, n;
+      int64_t srb, nrb = 0;
+      int32_t sli, nli = 0;
+      int32_t n = it.next(srb, sli);
       int s = 0, k = 0;
       uint32_t ph = 0;
-      while ((n = it.next(srb, sli)) > 0) {
+      while (n > 0) {
+        const int32_t nn = it.next(nrb, nli);
         if (k >= NST) mbar_wait(&empty[s], ph ^ 1u);
         if (p.trace && k < 32) p.trace[cta * 256 + 64 + k] = gtime();
+        const bool code = sli < g.nss;
+        uint32_t fl = 0;
+        if (nn == 0 || nrb != srb) fl |= kRbEnd;
+        else if (code && nli < g.nss && group_of(p, nli) == group_of(p, sli + n - 1)) fl |= kGroupCont;
+        asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(smem_addr(&desc[s])), "r"((uint32_t)srb),
+                     "r"((uint32_t)(sli & 0xFFFF) | ((uint32_t)n << 16) | (fl << 24)) : "memory");
         uint8_t* st = ring + (size_t)s * p.stage_bytes;
         const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
-        if (sli < g.nss) {
-          const int gi0 = group_of(p, sli);
-          const int ngrp = group_of(p, sli + n - 1) - gi0 + 1;
-          mbar_expect_tx(&full[s], cbytes + (uint32_t)n * (tile_bytes + sum_bytes) + (uint32_t)(ngrp * kSZBlockBytes));
+        if (code) {
+          mbar_expect_tx(&full[s], cbytes + (uint32_t)n * tile_bytes);
           bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
           bulk_g2s(st + p.tile_off, p.tiles + (int64_t)sli * tile_bytes, (uint32_t)n * tile_bytes, &full[s], pol_x);
-          bulk_g2s(st + p.sum_off, p.sums + (int64_t)sli * p.Bp, (uint32_t)n * sum_bytes, &full[s], pol_x);
-          bulk_g2s(st + p.sz_off, p.blob + g.sz_off + (srb * g.G + gi0) * kSZBlockBytes,
-                   (uint32_t)(ngrp * kSZBlockBytes), &full[s], pol);
         } else {
           mbar_expect_tx(&full[s], cbytes);
           bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
         }
         ++k;
         if (++s == NST) { s = 0; ph ^= 1u; }
+        srb = nrb;
+        sli = nli;
+        n = nn;
       }
+      // terminal descriptor: consumers leave their loops
+      if (k >= NST) mbar_wait(&empty[s], ph ^ 1u);
+      asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(smem_addr(&desc[s])), "r"(0u) : "memory");
+      mbar_arrive(&full[s]);
     }
   } else if (warp < C::kDecodeWarps) {
     // ==================================================================== decode
     // Warpgroup wg decodes a contiguous share (<= kIPW items of 128 rows x 64
     // codes) of every code stage into one of its two TMEM A buffers and
-    // publishes the buffer to its MMA warp (afull); it comes back via aempty.
+    // publishes it to its MMA warp: afull + a mailbox note {stage, share, flags}.
+    // Every code stage is published (possibly with no items) so the MMA warp
+    // sees each group end; a note with n == 0 ends the MMA warp.  One warp per
+    // warpgroup polls the mbarriers, the others wait on a named barrier.
     const int wg = warp >> 2, q = warp & 3;
     const int row = q * 32 + lane;                      // TMEM lane / row inside the row-block
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(wg * 2 * C::kABuf);
-    const uint32_t ss = (uint32_t)g.ss_bytes;
+    constexpr uint32_t kSS = (uint32_t)kRowBlock * (BITS == 3 ? 6 : 8) * 4;   // bytes per super-step record
     constexpr uint32_t kHiStride = BITS == 3 ? 8u : 16u;   // words 4.. of a row
+    const Shifts sh = make_shifts();
+    const int nss = g.nss;
+    const int bar_id = 3 + wg;
     uint32_t acnt = 0;                                  // A buffers published
-    StageIter it;
-    it.init(g, i0, i1, p.cap);
-    int64_t srb;
-    int32_t sli, n;
     int s = 0;
     uint32_t ph = 0;
-    int kst = 0;
-    while ((n = it.next(srb, sli)) > 0) {
-      mbar_wait(&full[s], ph);
-      if (p.trace && warp == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 192 + kst] = gtime();
-      int lo, hi;
-      share(n, wg, DWG, lo, hi);
-      if (sli < g.nss && lo < hi) {
+    for (;;) {
+      if (q == 0) mbar_wait(&full[s], ph);
+      named_sync(bar_id, 128);
+      const StageDesc d = load_desc(&desc[s]);
+      const bool code = d.n > 0 && d.li < nss;
+      if (code || d.n == 0) {
         const uint32_t buf = acnt & 1u;
-        if (acnt >= 2) mbar_wait(&aempty[wg * 2 + buf], ((acnt >> 1) & 1u) ^ 1u);
-        if (p.trace && warp == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 18 + kst] = gtime();
+        if (acnt >= 2) {
+          if (q == 0) mbar_wait(&aempty[wg * 2 + buf], ((acnt >> 1) & 1u) ^ 1u);
+          named_sync(bar_id, 128);
+        }
         ++acnt;
-        tc_fence_after();
-        const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
-        uint32_t a_lo = sbase + (uint32_t)lo * ss + (uint32_t)row * 16u;
-        uint32_t a_hi = sbase + (uint32_t)lo * ss + 2048u + (uint32_t)row * kHiStride;
-        uint32_t tcol = trow + buf * (uint32_t)C::kABuf;
-        for (int pi = lo; pi < hi; ++pi, a_lo += ss, a_hi += ss, tcol += C::kACols) {
-          uint32_t w[8];
-          {
-            const uint4 a = lds128(a_lo);
+        int lo = 0, hi = 0;
+        if (code) {
+          share<DWG>(d.n, wg, lo, hi);
+          tc_fence_after();
+          const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
+          const uint32_t a_lo = sbase + (uint32_t)lo * kSS + (uint32_t)row * 16u;
+          const uint32_t a_hi = sbase + (uint32_t)lo * kSS + 2048u + (uint32_t)row * kHiStride;
+          const uint32_t tcol = trow + buf * (uint32_t)C::kABuf;
+          auto item = [&](int t) {
+            uint32_t w[8];
+            const uint4 a = lds128(a_lo + t * kSS);
             w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
             if (BITS == 3) {
-              const uint2 b = lds64(a_hi);
+              const uint2 b = lds64(a_hi + t * kSS);
               w[4] = b.x; w[5] = b.y;
             } else {
-              const uint4 b = lds128(a_hi);
+              const uint4 b = lds128(a_hi + t * kSS);
               w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
             }
+            uint32_t o[16];
+            decode_row<BITS>(w, o, sh);
+            tc_st16(tcol + t * C::kACols, o);
+          };
+          if (p.exp == 3) {
+          } else if (hi - lo == C::kIPW) {   // full share: unrolled, immediate offsets
+#pragma unroll
+            for (int t = 0; t < C::kIPW; ++t) item(t);
+          } else {
+            for (int t = 0; t < hi - lo; ++t) item(t);
           }
-          uint32_t o[16];
-          decode_row<BITS>(w, o);
-          tc_st16(tcol, o);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
         }
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
+        if (q == 0 && lane == 0)
+          mbox[wg * 2 + buf] = make_uint4((uint32_t)s, (uint32_t)(uint16_t)d.li,
+                                          (uint32_t)d.n | ((uint32_t)lo << 8) | ((uint32_t)hi << 16) | ((uint32_t)d.flags << 24),
+                                          (uint32_t)d.rb);
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[wg * 2 + buf]);
+        if (d.n == 0) break;
+      } else if (q == 0 && lane == 0) {
+        mbar_arrive(&empty[s]);   // weak stage: on behalf of this warpgroup's MMA warp, which never sees it
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
-      if (p.trace && warp == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 96 + kst] = gtime();
-      ++kst;
       if (++s == NST) { s = 0; ph ^= 1u; }
     }
   } else if (warp >= C::kMmaWarp0) {
     // ==================================================================== MMA issue (one warp per warpgroup)
+    // Driven by the decode warpgroup's notes (afull + mailbox).  The whole warp
+    // runs this (warp-uniform control flow); one elected lane issues each
+    // tcgen05.mma / commit.
     const int wg = warp - C::kMmaWarp0;
-    if (lane == 0) {
-      uint32_t acnt = 0, dcnt = 0;
-      bool open = false;          // D[dcnt & 1] holds a partial group sum
-      const uint32_t a_wg = tmem + (uint32_t)(wg * 2 * C::kABuf);
-      constexpr uint32_t kLbo = (NN / 8) * 128;        // K-adjacent core matrices
-      StageIter it;
-      it.init(g, i0, i1, p.cap);
-      int64_t crb, nrb = -1;
-      int32_t cli, nli = 0;
-      int32_t cn = it.next(crb, cli);
-      int s = 0, kst = 0;
-      while (cn > 0) {
-        const int32_t nn = it.next(nrb, nli);
-        if (cli < g.nss) {
-          const uint32_t stile = smem_addr(ring + (size_t)s * p.stage_bytes) + (uint32_t)p.tile_off;
-          int lo, hi;
-          share(cn, wg, DWG, lo, hi);
-          uint32_t buf = 0;
-          if (lo < hi) {
-            buf = acnt & 1u;
-            mbar_wait(&afull[wg * 2 + buf], (acnt >> 1) & 1u);
-            if (p.trace && wg == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
-            ++acnt;
-            tc_fence_after();
-          }
-          for (int pa = 0; pa < cn;) {
-            const Seg sg = segment(p, pa, cn, cli, crb, nn, nrb, nli);
-            const int a0 = sg.pa > lo ? sg.pa : lo, a1 = sg.pb + 1 < hi ? sg.pb + 1 : hi;
-            for (int pi = a0; pi < a1; ++pi) {
-              const uint32_t dbuf = dcnt & 1u;
-              if (!open && dcnt >= 2) mbar_wait(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
-              const uint32_t a_t = a_wg + buf * (uint32_t)C::kABuf + (uint32_t)(pi - lo) * C::kACols;
-              const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * NN);
-              const uint32_t tb = stile + (uint32_t)pi * tile_bytes;
-#pragma unroll
-              for (int j = 0; j < 2; ++j)   // K = 32 columns each: TMEM columns 8j.., core-matrix K-chunks 2j, 2j+1
-                tc_mma_i8(d_t, a_t + 8 * j, umma_desc(tb + j * 2 * kLbo, kLbo, 128), idesc_i8<NN>(),
-                          (open || j > 0) ? 1u : 0u);
-              open = true;
-            }
-            if (sg.ends && open) {
-              tc_commit(&dfull[wg * 2 + (dcnt & 1u)]);
-              ++dcnt;
-              open = false;
-            }
-            pa = sg.pb + 1;
-          }
-          if (lo < hi) tc_commit(&aempty[wg * 2 + buf]);   // buffer consumed once these MMAs complete
+    uint32_t acnt = 0, dcnt = 0;
+    bool open = false;          // D[dcnt & 1] holds a partial group sum
+    const uint32_t a_wg = tmem + (uint32_t)(wg * 2 * C::kABuf);
+    constexpr uint32_t kLbo = (NN / 8) * 128;          // K-adjacent core matrices
+    const uint32_t ring0 = smem_addr(ring) + (uint32_t)p.tile_off;
+    int kst = 0;
+    long long c_wait = 0, c_issue = 0, c_commit = 0, c_mma = 0;   // trace only
+    for (;;) {
+      const uint32_t buf = acnt & 1u;
+      const long long t0 = clock64();
+      mbar_wait(&afull[wg * 2 + buf], (acnt >> 1) & 1u);
+      const long long t1 = clock64();
+      c_wait += t1 - t0;
+      ++acnt;
+      const uint4 note = mbox[wg * 2 + buf];
+      StageDesc d;
+      d.n = (uint8_t)(note.z & 0xFF);
+      if (d.n == 0) break;
+      d.li = (int16_t)note.y;
+      d.flags = (uint8_t)(note.z >> 24);
+      d.rb = (int32_t)note.w;
+      const int s = (int)note.x, lo = (int)((note.z >> 8) & 0xFF), hi = (int)((note.z >> 16) & 0xFF);
+      if (p.trace && wg == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
+      tc_fence_after();
+      const uint32_t stile = ring0 + (uint32_t)s * (uint32_t)p.stage_bytes;
+      if (!p.g.group && hi - lo == C::kIPW) {
+        // common case: one scale group, full share -> one asm block, one elect
+        const uint32_t dbuf = dcnt & 1u;
+        if (!open && dcnt >= 2) mbar_wait(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
+        tc_mma_i8_stage<C::kIPW, NN * kSuperStep, kLbo>(
+            tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * NN), a_wg + buf * (uint32_t)C::kABuf,
+            umma_desc(stile + (uint32_t)lo * tile_bytes, kLbo, 128), idesc_i8<NN>(), open ? 1u : 0u);
+        open = true;
+        c_mma += 2 * C::kIPW;
+        if (!(d.flags & kGroupCont)) {
+          tc_commit_elect(&dfull[wg * 2 + dbuf]);
+          ++dcnt;
+          open = false;
         }
-        tc_commit(&empty[s]);   // the stage's digit tiles are free once these MMAs completed
-        if (p.trace && wg == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
-        ++kst;
-        if (++s == NST) s = 0;
-        crb = nrb;
-        cli = nli;
-        cn = nn;
+      } else
+      for (int pa = 0; pa < d.n;) {
+        const Seg sg = segment(p, pa, d);
+        const int a0 = sg.pa > lo ? sg.pa : lo, a1 = sg.pb + 1 < hi ? sg.pb + 1 : hi;
+        for (int pi = a0; pi < a1; ++pi) {
+          const uint32_t dbuf = dcnt & 1u;
+          if (!open && dcnt >= 2) mbar_wait(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
+          const uint32_t a_t = a_wg + buf * (uint32_t)C::kABuf + (uint32_t)(pi - lo) * C::kACols;
+          const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * NN);
+          const uint32_t tb = stile + (uint32_t)pi * tile_bytes;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)   // K = 32 columns each: TMEM columns 8j.., core-matrix K-chunks 2j, 2j+1
+            tc_mma_i8_elect(d_t, a_t + 8 * j, umma_desc(tb + j * 2 * kLbo, kLbo, 128), idesc_i8<NN>(),
+                            (open || j > 0) ? 1u : 0u);
+          open = true;
+          c_mma += 2;
+        }
+        if (sg.ends && open) {
+          tc_commit_elect(&dfull[wg * 2 + (dcnt & 1u)]);
+          ++dcnt;
+          open = false;
+        }
+        pa = sg.pb + 1;
       }
+      const long long t2 = clock64();
+      tc_commit_elect(&aempty[wg * 2 + buf]);   // A buffer consumed once these MMAs complete
+      tc_commit_elect(&empty[s]);                // ... and the stage's digit tiles
+      const long long t3 = clock64();
+      c_issue += t2 - t1;
+      c_commit += t3 - t2;
+      if (p.trace && wg == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
+      ++kst;
+    }
+    if (p.trace && lane == 0) {
+      p.trace[cta * 256 + 1 + wg] = (unsigned long long)c_wait;
+      p.trace[cta * 256 + 5 + wg] = (unsigned long long)c_issue;
+      p.trace[cta * 256 + 9 + wg * 0] = (unsigned long long)c_commit;
+      p.trace[cta * 256 + 52] = (unsigned long long)c_mma;
     }
   } else {
     // ==================================================================== epilogue
@@ -514,46 +644,66 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
     named_sync(2, 128);
     constexpr double kPow256[6] = {1.0, 256.0, 65536.0, 16777216.0, 4294967296.0, 1099511627776.0};
     float tot[MAXB];
-    long long sacc[MAXB];                                // sum over the open group's items of x * 2^24
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b) { tot[b] = 0.f; sacc[b] = 0; }
+    for (int b = 0; b < MAXB; ++b) tot[b] = 0.f;
     uint32_t dcnt[DWG];
 #pragma unroll
     for (int w = 0; w < DWG; ++w) dcnt[w] = 0;
     uint32_t part = 0;                                   // warpgroups with items in the open group
-    int kst = 0;
-    StageIter it;
-    it.init(g, i0, i1, p.cap);
-    int64_t crb, nrb = -1;
-    int32_t cli, nli = 0;
-    int32_t cn = it.next(crb, cli);
+    int gfirst = -1;                                     // first item (li) of the open group in this CTA
+    int kst = 0, rr = 0;
     int s = 0;
     uint32_t ph = 0;
-    while (cn > 0) {
-      const int32_t nn = it.next(nrb, nli);
-      mbar_wait(&full[s], ph);
-      const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
-      if (cli < g.nss) {
-        const int gi0 = group_of(p, cli);
-        for (int pa = 0; pa < cn;) {
-          const Seg sg = segment(p, pa, cn, cli, crb, nn, nrb, nli);
+    for (;;) {
+      if (q == 0) mbar_wait(&full[s], ph);
+      named_sync(2, 128);
+      const StageDesc d = load_desc(&desc[s]);
+      if (d.n == 0) break;
+      const bool code = d.li < g.nss;
+      if (code) {
+        // nothing in a code stage's shared memory is needed here: release it now
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        for (int pa = 0; pa < d.n;) {
+          const Seg sg = segment(p, pa, d);
+          if (gfirst < 0) gfirst = d.li + sg.pa;
 #pragma unroll
           for (int w = 0; w < DWG; ++w) {
             int lo, hi;
-            share(cn, w, DWG, lo, hi);
+            share<DWG>(d.n, w, lo, hi);
             if (lo <= sg.pb && hi > sg.pa) part |= 1u << w;
           }
-          for (int pi = sg.pa; pi <= sg.pb; ++pi) {
-            const uint32_t sp = sbase + (uint32_t)p.sum_off + (uint32_t)pi * sum_bytes;
-#pragma unroll
-            for (int b = 0; b < MAXB; ++b)
-              if (b < p.B) {
-                const uint2 v = lds64(sp + b * 8);
-                sacc[b] += (long long)(((unsigned long long)v.y << 32) | v.x);
-              }
-          }
           if (sg.ends) {
-            const __half2 szv = u2h(lds32(sbase + p.sz_off + (sg.gi - gi0) * kSZBlockBytes + row * 4));
+            // x * 2^24 summed over the group's items (exact, from the digit pass)
+            const int glast = d.li + sg.pb, cnt = glast - gfirst + 1;
+            long long S[MAXB];
+#pragma unroll
+            for (int b = 0; b < MAXB; ++b) S[b] = 0;
+            if (cnt <= 8) {
+              for (int li = gfirst; li <= glast; ++li)
+#pragma unroll
+                for (int b = 0; b < MAXB; ++b)
+                  if (b < p.B) S[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
+            } else {
+              for (int li = gfirst + et; li <= glast; li += 128)
+#pragma unroll
+                for (int b = 0; b < MAXB; ++b)
+                  if (b < p.B) S[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
+              long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
+#pragma unroll
+              for (int b = 0; b < MAXB; ++b) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) S[b] += __shfl_xor_sync(0xffffffffu, S[b], o);
+                if (lane == 0) rd[q * OWQ_MAX_BATCH + b] = S[b];
+              }
+              named_sync(2, 128);
+#pragma unroll
+              for (int b = 0; b < MAXB; ++b)
+                S[b] = rd[b] + rd[OWQ_MAX_BATCH + b] + rd[2 * OWQ_MAX_BATCH + b] + rd[3 * OWQ_MAX_BATCH + b];
+              ++rr;
+            }
+            const __half2 szv = u2h(__ldg(reinterpret_cast<const unsigned int*>(
+                p.blob + g.sz_off + ((int64_t)d.rb * g.G + sg.gi) * kSZBlockBytes + row * 4)));
             const float s_g = __low2float(szv);
             const double z_g = (double)__high2float(szv);
             double dacc[MAXB];
@@ -568,12 +718,12 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
                 const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * NN);
 #pragma unroll
                 for (int c16 = 0; c16 < (MAXB * kDigits + 15) / 16; ++c16) {
-                  uint32_t d[16];
-                  tc_ld16(tcol + 16 * c16, d);
+                  uint32_t dd[16];
+                  tc_ld16(tcol + 16 * c16, dd);
 #pragma unroll
                   for (int j = 0; j < 16; ++j) {
                     const int col = 16 * c16 + j, b = col / kDigits, i = col % kDigits;
-                    if (b < MAXB) dacc[b] += (double)(int)d[j] * kPow256[i];
+                    if (b < MAXB) dacc[b] += (double)(int)dd[j] * kPow256[i];
                   }
                 }
                 tc_fence_before();
@@ -583,18 +733,18 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
               }
             }
 #pragma unroll
-            for (int b = 0; b < MAXB; ++b) {
-              tot[b] = fmaf(s_g, (float)((dacc[b] - z_g * (double)sacc[b]) * 5.9604644775390625e-08), tot[b]);
-              sacc[b] = 0;
-            }
+            for (int b = 0; b < MAXB; ++b)
+              tot[b] = fmaf(s_g, (float)((dacc[b] - z_g * (double)S[b]) * 5.9604644775390625e-08), tot[b]);
             part = 0;
+            gfirst = -1;
           }
           pa = sg.pb + 1;
         }
       } else {
         // weak chunks: fp16 weak columns x gathered activations, fp32 (unscaled)
-        for (int pi = 0; pi < cn; ++pi) {
-          const int gch = cli - g.nss + pi;
+        const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
+        for (int pi = 0; pi < d.n; ++pi) {
+          const int gch = d.li - g.nss + pi;
           float v[8];
           if (gch < g.nfull) {
             const uint4 a = lds128(sbase + pi * kWeakChunkBytes + row * 16);
@@ -626,16 +776,17 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
             }
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
       if (p.trace && et == 0 && kst < 32) p.trace[cta * 256 + 160 + kst] = gtime();
       ++kst;
       if (++s == NST) { s = 0; ph ^= 1u; }
 
-      if (nn == 0 || nrb != crb) {
-        // -------------------------------------------------- finish row-block crb
+      if (d.flags & kRbEnd) {
+        // -------------------------------------------------- finish row-block d.rb
         if (p.trace && et == 0) p.trace[cta * 256 + 50] = gtime();
+        const int64_t crb = d.rb;
         const int64_t ifirst = crb * n_rb, ilast = ifirst + n_rb - 1;
         const bool whole = ifirst >= i0 && ilast < i1;
         const int64_t grow = crb * kRowBlock + row;
@@ -681,9 +832,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
         for (int b = 0; b < MAXB; ++b) tot[b] = 0.f;
         if (p.trace && et == 0) p.trace[cta * 256 + 56] = gtime();
       }
-      crb = nrb;
-      cli = nli;
-      cn = nn;
     }
   }
   // teardown: every role is done with TMEM
@@ -788,30 +936,28 @@ template <int BITS, int NN>
 static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   using C = Cfg<BITS, NN>;
   Params p = p0;
-  const int64_t tile_bytes = (int64_t)NN * kSuperStep, sum_bytes = (int64_t)p.Bp * 8;
+  const int64_t tile_bytes = (int64_t)NN * kSuperStep;
   int dev = 0, maxsmem = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t fixed = (((size_t)p.B * p.g.kpad + 7) & ~(size_t)7) * 2 + 512;
+  // x at the weak columns, the S reduction buffer, barriers + stage descriptors
+  const size_t fixed = (((size_t)p.B * p.g.kpad + 7) & ~(size_t)7) * 2 + 2 * 4 * OWQ_MAX_BATCH * 8 + 512;
   const int64_t avail = (int64_t)maxsmem - (int64_t)fixed - 1024;
-  // items per warpgroup per stage: fill the TMEM slot ring, but keep >= 4 stages
-  const int64_t per_item = std::max<int64_t>(p.g.ss_bytes, kWeakChunkBytes) + tile_bytes + sum_bytes;
+  // items per warpgroup per stage: fill the TMEM A buffers, but keep >= 4 stages
+  const int64_t per_item = std::max<int64_t>(p.g.ss_bytes, kWeakChunkBytes) + tile_bytes;
   static const int ipw_env = getenv("OWQ_IPW") ? atoi(getenv("OWQ_IPW")) : 0;   // experiments
   int ipw = ipw_env > 0 && ipw_env < C::kIPW ? ipw_env : C::kIPW;
   while (ipw > 1 && 4 * (C::DWG * ipw * per_item + 2048) > avail) --ipw;
   p.cap = C::DWG * ipw;
   p.code_bytes = (int32_t)std::max<int64_t>((int64_t)p.cap * p.g.ss_bytes, (int64_t)p.cap * kWeakChunkBytes);
   p.tile_off = p.code_bytes;
-  p.sum_off = p.tile_off + (int32_t)(p.cap * tile_bytes);
-  p.sz_off = p.sum_off + (int32_t)((p.cap * sum_bytes + 15) / 16 * 16);
-  const int sz_blocks = p.g.group ? (int)(p.cap * kSuperStep / p.g.group + 2) : 1;
-  p.stage_bytes = (p.sz_off + sz_blocks * kSZBlockBytes + 127) / 128 * 128;
-  int nst = (int)(avail / (p.stage_bytes + 16));
+  p.stage_bytes = (int32_t)((p.tile_off + p.cap * tile_bytes + 127) / 128 * 128);
+  int nst = (int)(avail / (p.stage_bytes + 24));
   static const int max_nst = getenv("OWQ_NST") ? atoi(getenv("OWQ_NST")) : 8;
   nst = std::min(nst, max_nst);
   if (nst < 2) return OWQ_ERR_UNSUPPORTED;     // too many weak columns / batch rows for shared memory
   p.nst = nst;
-  const size_t smem = (size_t)nst * p.stage_bytes + fixed + (size_t)nst * 16;
+  const size_t smem = (size_t)nst * p.stage_bytes + fixed + (size_t)nst * 24;
   auto kern = owq_gemv_kernel<BITS, NN>;
   static thread_local size_t configured = 0;
   if (configured < smem) {
@@ -873,6 +1019,8 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   if (trace_path && !trace_buf) cudaMalloc(&trace_buf, 4096 * 256 * 8);
   if (trace_buf) cudaMemsetAsync(trace_buf, 0, 4096 * 256 * 8, cs);
   p.trace = trace_buf;
+  static const int exp_env = getenv("OWQ_EXP") ? atoi(getenv("OWQ_EXP")) : 0;
+  p.exp = exp_env;
   p.group_log2 = 0;
   if (g.group) while ((kSuperStep << p.group_log2) < g.group) ++p.group_log2;
   const owq_status rs = g.bits == 3 ? launch_n<3>(p, grid, cs) : launch_n<4>(p, grid, cs);

@@ -28,3 +28,6 @@ for kk in range(0, 16):
         v = t[:, c]; v = v[v > 0]
         vals.append(f"{np.median(rel(v)):9.2f}" if len(v) else "        -")
     print(f" {kk:5d} " + " ".join(vals))
+print(" MMA warps (cycles, mean over CTAs): wait afull", [int(t[:, 1 + w].mean()) for w in range(4)],
+      " issue", [int(t[:, 5 + w].mean()) for w in range(4)], " commit(wg3)", int(t[:, 9].mean()), " MMAs(wg3)", int(t[:, 52].mean()))
+print(" kernel cycles ~", int((np.median(t[:, 62]) - np.median(t[:, 0])) * 1.9))
