@@ -55,6 +55,8 @@ static inline int mma_n_for(int B) {
 }
 static inline int batch_pad(int B) { return (B + 1) & ~1; }   // digit-sum rows (16-byte aligned runs)
 
+constexpr int kMaxGrid = 512;       // CTAs per launch (the span table rides in the kernel parameters)
+
 struct Params {
   const uint8_t* blob;
   const __half* x;
@@ -70,9 +72,12 @@ struct Params {
   int32_t cap;            // items per stage
   int32_t code_bytes;     // stage region for codes / weak chunks
   int32_t tile_off;       // digit tiles inside a stage
+  int32_t sum_off;        // per-item digit sums inside a stage (in-kernel digit mode)
+  int32_t x_off;          // raw x columns of the stage, B rows of cap*64 fp16 (in-kernel digit mode)
   int32_t stage_bytes;
   int64_t xK;             // row stride of x in elements
   int32_t group_log2;     // log2(group_size / 64)
+  int32_t span[kMaxGrid + 1];  // first item of each CTA (stream-K split, host-computed)
   unsigned long long* trace;   // experiments only (OWQ_TRACE)
   int32_t exp;                 // experiments only (OWQ_EXP): 3 = skip the TMEM stores
 };
@@ -176,7 +181,7 @@ __device__ __forceinline__ void tc_mma_i8_stage(uint32_t d_t, uint32_t a0, uint6
   "add.u32 a, a, 8;\n\t"                                                                           \
   "add.u64 b, b, %6/16;\n\t"                                                                       \
   "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a], b, %3, p;\n\t"
-  static_assert(IPW >= 1 && IPW <= 4, "IPW");
+  static_assert(IPW >= 1 && IPW <= 6, "IPW");
   if (IPW == 1)
     asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
                  "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) "}" ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc), "r"(acc),
@@ -189,10 +194,18 @@ __device__ __forceinline__ void tc_mma_i8_stage(uint32_t d_t, uint32_t a0, uint6
     asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
                  "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) "}" ::"r"(d_t), "r"(a0), "l"(b0),
                  "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
-  else
+  else if (IPW == 4)
     asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
                  "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) OWQ_MMA_T(3) "}" ::"r"(d_t),
                  "r"(a0), "l"(b0), "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
+  else if (IPW == 5)
+    asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) OWQ_MMA_T(3) OWQ_MMA_T(4) "}"
+                 ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
+  else
+    asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) OWQ_MMA_T(3) OWQ_MMA_T(4)
+                 OWQ_MMA_T(5) "}" ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
 #undef OWQ_MMA_T
 }
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_t, uint32_t a_t, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
@@ -300,15 +313,56 @@ __global__ void owq_x_digits_kernel(const __half* __restrict__ x, int64_t xK, in
   if (k == 0) sums[(int64_t)ss * Bp + b] = part[2 * b] + part[2 * b + 1];
 }
 
+// Balanced base-256 digits of X (|X| < 2^40) as the bytes of
+// (X + 0x808080808080) ^ 0x808080808080: byte i = b_i - 128 in two's complement
+// where b_i are the bytes of X + sum 128*256^i (carries included), so
+// sum_i (int8)byte_i 256^i = X.
+__device__ __forceinline__ unsigned long long digit_bytes(long long X) {
+  return (unsigned long long)(X + 0x808080808080LL) ^ 0x808080808080ULL;
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+// w[i] = digit i of the 4 values (byte j = value j), i < 6
+__device__ __forceinline__ void digits4(const unsigned long long* v, uint32_t* w) {
+  const uint32_t l0 = (uint32_t)v[0], l1 = (uint32_t)v[1], l2 = (uint32_t)v[2], l3 = (uint32_t)v[3];
+  const uint32_t h0 = (uint32_t)(v[0] >> 32), h1 = (uint32_t)(v[1] >> 32), h2 = (uint32_t)(v[2] >> 32),
+                 h3 = (uint32_t)(v[3] >> 32);
+  const uint32_t a01 = prmt(l0, l1, 0x5140), a23 = prmt(l2, l3, 0x5140);   // bytes 0,1 interleaved
+  const uint32_t b01 = prmt(l0, l1, 0x7362), b23 = prmt(l2, l3, 0x7362);   // bytes 2,3 interleaved
+  const uint32_t c01 = prmt(h0, h1, 0x5140), c23 = prmt(h2, h3, 0x5140);   // bytes 4,5 interleaved
+  w[0] = prmt(a01, a23, 0x5410); w[1] = prmt(a01, a23, 0x7632);
+  w[2] = prmt(b01, b23, 0x5410); w[3] = prmt(b01, b23, 0x7632);
+  w[4] = prmt(c01, c23, 0x5410); w[5] = prmt(c01, c23, 0x7632);
+}
+
+// x rows whose stride or base breaks 16-byte TMA alignment are first copied
+// into a zero-padded [B][Kp] buffer in the workspace (Kp = K rounded up to 64).
+__global__ void owq_pad_x_kernel(const __half* __restrict__ x, __half* __restrict__ xp, int B, int K, int Kp) {
+  const int64_t n = (int64_t)B * Kp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / Kp), c = (int)(i - (int64_t)b * Kp);
+    xp[i] = c < K ? x[(int64_t)b * K + c] : __float2half(0.f);
+  }
+}
+
 // group of code item li (row-block relative super-step index)
 __device__ __forceinline__ int group_of(const Params& p, int li) { return p.g.group ? (li >> p.group_log2) : 0; }
 
-// Per MMA-N class: decode warpgroups, items per warpgroup per stage, largest batch.
-// Each warpgroup owns two TMEM A buffers (ping-pong) of kIPW items.
-template <int BITS, int NN>
+// Per (MMA-N class, decode warpgroups): items per warpgroup per stage, largest
+// batch.  Each warpgroup owns two TMEM A buffers (ping-pong) of kIPW items and
+// two D accumulators of NN columns; kIPW is what fits in the 512 TMEM columns.
+template <int BITS, int NN, int DWG_>
 struct Cfg {
-  static constexpr int DWG = NN <= 32 ? 4 : 2;
-  static constexpr int kIPW = NN <= 16 ? 3 : NN == 32 ? 2 : NN == 64 ? 4 : 2;
+  static constexpr int DWG = DWG_;
+  // In-kernel digit mode (decode warps turn the stage's raw x into digit tiles,
+  // no pre-pass) is implemented but off: measured slower on B200 (12288^2 B=1:
+  // 28.2 us vs 24.0 us) because it lengthens the decode warps' stage.
+  static constexpr bool kInDig = false;
+  static constexpr int kIPW0 = (512 - 2 * DWG * NN) / (2 * DWG * 16);
+  static constexpr int kIPW = kIPW0 > 6 ? 6 : kIPW0;
   static constexpr int kMaxB = NN == 8 ? 1 : NN == 16 ? 2 : NN == 32 ? 5 : NN == 64 ? 10 : 16;
   static constexpr int kDecodeWarps = 4 * DWG;            // DWG decode warpgroups
   static constexpr int kEpiWarp0 = kDecodeWarps;          // 4 epilogue warps (warp % 4 = TMEM lane quarter)
@@ -376,9 +430,9 @@ __device__ __forceinline__ StageDesc load_desc(const StageDesc* d) {
   return r;
 }
 
-template <int BITS, int NN>
-__global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(const Params p) {
-  using C = Cfg<BITS, NN>;
+template <int BITS, int NN, int DWG_>
+__global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_kernel(const Params p) {
+  using C = Cfg<BITS, NN, DWG_>;
   constexpr int DWG = C::DWG, MAXB = C::kMaxB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geo& g = p.g;
@@ -394,8 +448,9 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
   uint64_t* aempty = afull + DWG * 2;  // [DWG][2]  MMA done reading it
   uint64_t* dfull = aempty + DWG * 2;  // [DWG][2]  group accumulator complete
   uint64_t* dempty = dfull + 2 * DWG;  // [DWG][2]  epilogue drained it
-  StageDesc* desc = reinterpret_cast<StageDesc*>(dempty + 2 * DWG);   // [NST]
-  uint4* mbox = reinterpret_cast<uint4*>(desc + NST + (NST & 1));     // [DWG][2] decode -> MMA stage notes
+  uint64_t* tready = dempty + 2 * DWG;  // [NST]  digit tiles of the stage written (in-kernel digit mode, 4 warps)
+  StageDesc* desc = reinterpret_cast<StageDesc*>(tready + NST);       // [NST]
+  uint4* mbox = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(desc + NST) + 15) & ~(uintptr_t)15);   // [DWG][2] decode -> MMA notes
   int64_t* span = reinterpret_cast<int64_t*>(mbox + 2 * DWG);         // [2] this CTA's item range
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(span + 2);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
@@ -403,10 +458,9 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
   const int64_t grid = gridDim.x, cta = blockIdx.x;
   if (threadIdx.x == 0) {
     if (p.trace) p.trace[cta * 256 + 0] = gtime();
-    // the host caps the grid so that every CTA's byte window holds an item start
-    span[0] = cta_first_item(g, grid, cta);
-    span[1] = cta_first_item(g, grid, cta + 1);
-    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); }
+    span[0] = p.span[cta];
+    span[1] = p.span[cta + 1];
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); mbar_init(&tready[s], 4); }
     for (int i = 0; i < 2 * DWG; ++i) {
       mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4);
     }
@@ -448,10 +502,18 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
                      "r"((uint32_t)(sli & 0xFFFF) | ((uint32_t)n << 16) | (fl << 24)) : "memory");
         uint8_t* st = ring + (size_t)s * p.stage_bytes;
         const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
-        if (code) {
+        if (code && !C::kInDig) {
           mbar_expect_tx(&full[s], cbytes + (uint32_t)n * tile_bytes);
           bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
           bulk_g2s(st + p.tile_off, p.tiles + (int64_t)sli * tile_bytes, (uint32_t)n * tile_bytes, &full[s], pol_x);
+        } else if (code) {
+          // codes + the x columns of the stage (x rows are 16-byte aligned, K % 8 == 0: host-checked)
+          const int64_t col0 = (int64_t)sli * kSuperStep;
+          const int64_t xc = p.xK - col0 < (int64_t)n * kSuperStep ? p.xK - col0 : (int64_t)n * kSuperStep;
+          mbar_expect_tx(&full[s], cbytes + (uint32_t)(p.B * xc * 2));
+          bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
+          for (int b = 0; b < p.B; ++b)
+            bulk_g2s(st + p.x_off + b * p.cap * kSuperStep * 2, p.x + (int64_t)b * p.xK + col0, (uint32_t)(xc * 2), &full[s], pol_x);
         } else {
           mbar_expect_tx(&full[s], cbytes);
           bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
@@ -528,11 +590,42 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
           } else {
             for (int t = 0; t < hi - lo; ++t) item(t);
           }
+          if (C::kInDig) {
+            // digit tiles of this warpgroup's items: warp q converts items lo+q, lo+q+4, ..
+            // lane = (batch row bb, columns 4*nl .. 4*nl+3)
+            const int nl = lane & 15, bb = lane >> 4;
+            for (int pi = lo + q; pi < hi; pi += 4) {
+              const int64_t col0 = (int64_t)(d.li + pi) * kSuperStep + nl * 4;
+              const uint32_t tb = sbase + (uint32_t)p.tile_off + (uint32_t)pi * (uint32_t)(NN * kSuperStep) +
+                                  (uint32_t)(nl >> 2) * (NN / 8) * 128 + (uint32_t)(nl & 3) * 4;
+              if (bb < p.B) {
+                const uint2 xr = lds64(sbase + (uint32_t)p.x_off + (uint32_t)(bb * p.cap * kSuperStep + pi * kSuperStep + nl * 4) * 2u);
+                const uint32_t xh[2] = {xr.x, xr.y};
+                unsigned long long v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const __half h = __ushort_as_half((unsigned short)(xh[j >> 1] >> (16 * (j & 1))));
+                  v[j] = digit_bytes(col0 + j < g.K ? x_fixed(h) : 0);
+                }
+                uint32_t wd[kDigits];
+                digits4(v, wd);
+#pragma unroll
+                for (int i = 0; i < kDigits; ++i) {
+                  const int n = kDigits * bb + i;
+                  asm volatile("st.shared.u32 [%0], %1;" ::"r"(tb + (uint32_t)((n >> 3) * 128 + (n & 7) * 16)), "r"(wd[i]) : "memory");
+                }
+              }
+              if (bb == 0)
+                for (int n = kDigits * p.B; n < NN; ++n)
+                  asm volatile("st.shared.u32 [%0], %1;" ::"r"(tb + (uint32_t)((n >> 3) * 128 + (n & 7) * 16)), "r"(0u) : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // tiles -> async proxy (MMA)
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
         }
         if (q == 0 && lane == 0)
-          mbox[wg * 2 + buf] = make_uint4((uint32_t)s, (uint32_t)(uint16_t)d.li,
+          mbox[wg * 2 + buf] = make_uint4((uint32_t)s | (ph << 31), (uint32_t)(uint16_t)d.li,
                                           (uint32_t)d.n | ((uint32_t)lo << 8) | ((uint32_t)hi << 16) | ((uint32_t)d.flags << 24),
                                           (uint32_t)d.rb);
         __syncwarp();
@@ -572,7 +665,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
       d.li = (int16_t)note.y;
       d.flags = (uint8_t)(note.z >> 24);
       d.rb = (int32_t)note.w;
-      const int s = (int)note.x, lo = (int)((note.z >> 8) & 0xFF), hi = (int)((note.z >> 16) & 0xFF);
+      const int s = (int)(note.x & 0x7FFFFFFFu), lo = (int)((note.z >> 8) & 0xFF), hi = (int)((note.z >> 16) & 0xFF);
       if (p.trace && wg == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
       tc_fence_after();
       const uint32_t stile = ring0 + (uint32_t)s * (uint32_t)p.stage_bytes;
@@ -644,8 +737,9 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
     named_sync(2, 128);
     constexpr double kPow256[6] = {1.0, 256.0, 65536.0, 16777216.0, 4294967296.0, 1099511627776.0};
     float tot[MAXB];
+    long long sgrp[MAXB];                                // in-kernel digit mode: sum of the open group's digit sums
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b) tot[b] = 0.f;
+    for (int b = 0; b < MAXB; ++b) { tot[b] = 0.f; sgrp[b] = 0; }
     uint32_t dcnt[DWG];
 #pragma unroll
     for (int w = 0; w < DWG; ++w) dcnt[w] = 0;
@@ -660,26 +754,64 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
       const StageDesc d = load_desc(&desc[s]);
       if (d.n == 0) break;
       const bool code = d.li < g.nss;
+      const uint32_t sbase_e = smem_addr(ring + (size_t)s * p.stage_bytes);
+      (void)sbase_e;
       if (code) {
-        // nothing in a code stage's shared memory is needed here: release it now
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        long long sst[MAXB];   // this stage's digit sums of the items of each segment (in-kernel digit mode)
+        if (!C::kInDig) {
+          // nothing in a code stage's shared memory is needed here: release it now
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
         for (int pa = 0; pa < d.n;) {
           const Seg sg = segment(p, pa, d);
           if (gfirst < 0) gfirst = d.li + sg.pa;
+          if (d.n == p.cap && !p.g.group) {
+            part = (1u << DWG) - 1u;   // full stage, one segment: every warpgroup has items
+          } else {
 #pragma unroll
-          for (int w = 0; w < DWG; ++w) {
-            int lo, hi;
-            share<DWG>(d.n, w, lo, hi);
-            if (lo <= sg.pb && hi > sg.pa) part |= 1u << w;
+            for (int w = 0; w < DWG; ++w) {
+              int lo, hi;
+              share<DWG>(d.n, w, lo, hi);
+              if (lo <= sg.pb && hi > sg.pa) part |= 1u << w;
+            }
+          }
+          if (C::kInDig) {
+            // this thread's share of sum x * 2^24 over the segment's columns (raw x in the stage)
+            const int ncol = (sg.pb - sg.pa + 1) * kSuperStep;
+            const int64_t cbase = (int64_t)(d.li + sg.pa) * kSuperStep;
+#pragma unroll
+            for (int b = 0; b < MAXB; ++b)
+              if (b < p.B)
+                for (int c = et; c < ncol; c += 128) {
+                  const __half h = __ushort_as_half((unsigned short)(lds32(sbase_e + (uint32_t)p.x_off +
+                      (uint32_t)(b * p.cap * kSuperStep + sg.pa * kSuperStep + (c & ~1)) * 2u) >> (16 * (c & 1))));
+                  if (cbase + c < g.K) sgrp[b] += x_fixed(h);
+                }
           }
           if (sg.ends) {
-            // x * 2^24 summed over the group's items (exact, from the digit pass)
+            // x * 2^24 summed over the group's items (exact)
             const int glast = d.li + sg.pb, cnt = glast - gfirst + 1;
             long long S[MAXB];
 #pragma unroll
             for (int b = 0; b < MAXB; ++b) S[b] = 0;
-            if (cnt <= 8) {
+            if (C::kInDig) {
+              // block-reduce the threads' shares (the same for every row)
+              long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
+#pragma unroll
+              for (int b = 0; b < MAXB; ++b) {
+                long long v = sgrp[b];
+                sgrp[b] = 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) rd[q * OWQ_MAX_BATCH + b] = v;
+              }
+              named_sync(2, 128);
+#pragma unroll
+              for (int b = 0; b < MAXB; ++b)
+                S[b] = rd[b] + rd[OWQ_MAX_BATCH + b] + rd[2 * OWQ_MAX_BATCH + b] + rd[3 * OWQ_MAX_BATCH + b];
+              ++rr;
+            } else if (cnt <= 8) {
               for (int li = gfirst; li <= glast; ++li)
 #pragma unroll
                 for (int b = 0; b < MAXB; ++b)
@@ -740,6 +872,11 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
           }
           pa = sg.pb + 1;
         }
+        if (C::kInDig) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        (void)sst;
       } else {
         // weak chunks: fp16 weak columns x gathered activations, fp32 (unscaled)
         const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
@@ -804,7 +941,16 @@ __global__ void __launch_bounds__(Cfg<BITS, NN>::kThreads, 1) owq_gemv_kernel(co
           for (int b = 0; b < MAXB; ++b)
             if (b < p.B) __stcg(&p.partial[((crb + cta) * p.B + b) * kRowBlock + row], tot[b]);
           // pieces = CTAs cta_of(first item) .. cta_of(last item) (none is empty)
-          const int64_t c_first = cta_of_item(g, grid, ifirst), c_last = cta_of_item(g, grid, ilast);
+          // pieces = CTAs holding the first .. last item of the row-block (span table search)
+          auto cta_of = [&](int64_t item) {
+            int lo_c = 0, hi_c = (int)grid;   // span[lo_c] <= item < span[hi_c]
+            while (hi_c - lo_c > 1) {
+              const int mid = (lo_c + hi_c) >> 1;
+              if (p.span[mid] <= item) lo_c = mid; else hi_c = mid;
+            }
+            return (int64_t)lo_c;
+          };
+          const int64_t c_first = cta_of(ifirst), c_last = cta_of(ilast);
           const int npieces = (int)(c_last - c_first + 1);
           named_sync(2, 128);
           if (et == 0) {
@@ -928,13 +1074,14 @@ static size_t ws_partials(const Geo& g, int B, int64_t G) {
 }
 static size_t ws_tiles(const Geo& g, int B) { return (size_t)g.nss * mma_n_for(B) * kSuperStep; }
 static size_t ws_sums(const Geo& g, int B) { return (size_t)g.nss * batch_pad(B) * 8; }
+static size_t ws_xpad(const Geo& g, int B) { return ((size_t)B * g.nss * kSuperStep * 2 + 255) / 256 * 256; }
 static size_t ws_bytes_for(const Geo& g, int B, int64_t G) {
-  return ws_counters(g) + ws_partials(g, B, G) + ws_tiles(g, B) + ws_sums(g, B);
+  return ws_counters(g) + ws_partials(g, B, G) + ws_tiles(g, B) + ws_sums(g, B) + ws_xpad(g, B);
 }
 
-template <int BITS, int NN>
+template <int BITS, int NN, int DWG>
 static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
-  using C = Cfg<BITS, NN>;
+  using C = Cfg<BITS, NN, DWG>;
   Params p = p0;
   const int64_t tile_bytes = (int64_t)NN * kSuperStep;
   int dev = 0, maxsmem = 0;
@@ -944,21 +1091,24 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   const size_t fixed = (((size_t)p.B * p.g.kpad + 7) & ~(size_t)7) * 2 + 2 * 4 * OWQ_MAX_BATCH * 8 + 512;
   const int64_t avail = (int64_t)maxsmem - (int64_t)fixed - 1024;
   // items per warpgroup per stage: fill the TMEM A buffers, but keep >= 4 stages
-  const int64_t per_item = std::max<int64_t>(p.g.ss_bytes, kWeakChunkBytes) + tile_bytes;
+  const int64_t per_item = std::max<int64_t>(p.g.ss_bytes, kWeakChunkBytes) + tile_bytes +
+                           (C::kInDig ? p.Bp * 8 + p.B * kSuperStep * 2 : 0);
   static const int ipw_env = getenv("OWQ_IPW") ? atoi(getenv("OWQ_IPW")) : 0;   // experiments
   int ipw = ipw_env > 0 && ipw_env < C::kIPW ? ipw_env : C::kIPW;
   while (ipw > 1 && 4 * (C::DWG * ipw * per_item + 2048) > avail) --ipw;
   p.cap = C::DWG * ipw;
   p.code_bytes = (int32_t)std::max<int64_t>((int64_t)p.cap * p.g.ss_bytes, (int64_t)p.cap * kWeakChunkBytes);
   p.tile_off = p.code_bytes;
-  p.stage_bytes = (int32_t)((p.tile_off + p.cap * tile_bytes + 127) / 128 * 128);
-  int nst = (int)(avail / (p.stage_bytes + 24));
+  p.sum_off = p.tile_off + (int32_t)(p.cap * tile_bytes);
+  p.x_off = p.sum_off + (int32_t)((C::kInDig ? p.cap * p.Bp * 8 : 0) + 127) / 128 * 128;
+  p.stage_bytes = (int32_t)((p.x_off + (C::kInDig ? p.B * p.cap * kSuperStep * 2 : 0) + 127) / 128 * 128);
+  int nst = (int)(avail / (p.stage_bytes + 32));
   static const int max_nst = getenv("OWQ_NST") ? atoi(getenv("OWQ_NST")) : 8;
   nst = std::min(nst, max_nst);
   if (nst < 2) return OWQ_ERR_UNSUPPORTED;     // too many weak columns / batch rows for shared memory
   p.nst = nst;
-  const size_t smem = (size_t)nst * p.stage_bytes + fixed + (size_t)nst * 24;
-  auto kern = owq_gemv_kernel<BITS, NN>;
+  const size_t smem = (size_t)nst * p.stage_bytes + fixed + (size_t)nst * 32;
+  auto kern = owq_gemv_kernel<BITS, NN, DWG>;
   static thread_local size_t configured = 0;
   if (configured < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -968,7 +1118,7 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   kern<<<(unsigned)grid, C::kThreads, smem, stream>>>(p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
-    fprintf(stderr, "owq: launch of owq_gemv_kernel<%d,%d> (grid %lld, smem %zu) failed: %s\n", BITS, NN,
+    fprintf(stderr, "owq: launch of owq_gemv_kernel<%d,%d,%d> (grid %lld, smem %zu) failed: %s\n", BITS, NN, DWG,
             (long long)grid, smem, cudaGetErrorString(e));
     return OWQ_ERR_CUDA;
   }
@@ -977,12 +1127,16 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
 
 template <int BITS>
 static owq_status launch_n(const Params& p, int64_t grid, cudaStream_t cs) {
+  static const int dwg = getenv("OWQ_DWG") ? atoi(getenv("OWQ_DWG")) : 0;   // experiments (B = 1 only)
   switch (mma_n_for(p.B)) {
-    case 8: return launch<BITS, 8>(p, grid, cs);
-    case 16: return launch<BITS, 16>(p, grid, cs);
-    case 32: return launch<BITS, 32>(p, grid, cs);
-    case 64: return launch<BITS, 64>(p, grid, cs);
-    default: return launch<BITS, 96>(p, grid, cs);
+    case 8:
+      if (dwg == 2) return launch<BITS, 8, 2>(p, grid, cs);
+      if (dwg == 4) return launch<BITS, 8, 4>(p, grid, cs);
+      return launch<BITS, 8, 3>(p, grid, cs);
+    case 16: return launch<BITS, 16, 4>(p, grid, cs);
+    case 32: return launch<BITS, 32, 4>(p, grid, cs);
+    case 64: return launch<BITS, 64, 2>(p, grid, cs);
+    default: return launch<BITS, 96, 2>(p, grid, cs);
   }
 }
 
@@ -994,6 +1148,7 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   owq_status st = check_blob_cached(s, d_packed, g);
   if (st != OWQ_OK) return st;
   const int64_t grid = grid_for(g, grid_req);
+  if (grid > kMaxGrid || (int64_t)g.nrb * items_per_rb(g) >= (1ll << 31)) return OWQ_ERR_UNSUPPORTED;
   if (ws_bytes < ws_bytes_for(g, B, grid)) return OWQ_ERR_BUFFER_TOO_SMALL;
   Params p{};
   p.blob = (const uint8_t*)d_packed;
@@ -1006,14 +1161,27 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.tiles = tiles;
   p.sums = sums;
   p.g = g;
+  for (int64_t c = 0; c <= grid; ++c) p.span[c] = (int32_t)cta_first_item(g, grid, c);
   p.B = B;
   p.Bp = batch_pad(B);
   p.y_f32 = y_f32 ? 1 : 0;
   p.xK = g.K;
   cudaStream_t cs = (cudaStream_t)stream;
+  if (false) {   // in-kernel digit mode only (off): TMA of x needs 16-byte aligned rows
+    // in-kernel digit mode streams x with TMA: rows must be 16-byte aligned
+    __half* xp = (__half*)((uint8_t*)d_ws + ws_counters(g) + ws_partials(g, B, grid) + ws_tiles(g, B) + ws_sums(g, B));
+    const int Kp = g.nss * kSuperStep;
+    const int64_t n = (int64_t)B * Kp;
+    owq_pad_x_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, cs>>>(p.x, xp, B, g.K, Kp);
+    if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
+    p.x = xp;
+    p.xK = Kp;
+  }
   // x -> exact int8 digits in UMMA tile order, plus per-super-step digit sums
-  owq_x_digits_kernel<<<(unsigned)g.nss, 64 * p.Bp, 0, cs>>>(p.x, p.xK, B, p.Bp, g.K, mma_n_for(B), tiles, sums);
-  if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
+  {
+    owq_x_digits_kernel<<<(unsigned)g.nss, 64 * p.Bp, 0, cs>>>(p.x, p.xK, B, p.Bp, g.K, mma_n_for(B), tiles, sums);
+    if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
+  }
   static unsigned long long* trace_buf = nullptr;
   static const char* trace_path = getenv("OWQ_TRACE");
   if (trace_path && !trace_buf) cudaMalloc(&trace_buf, 4096 * 256 * 8);

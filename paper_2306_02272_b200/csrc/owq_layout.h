@@ -33,7 +33,20 @@ constexpr int kHeaderBytes = 256;
 constexpr int kSZBlockBytes = kRowBlock * 4;                  // 128 x (s, z) fp16 pairs
 constexpr uint32_t kMagic = 0x4257514Fu;                      // "OQWB"
 
-OWQ_HD int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+// floor(a / b) for 0 <= a < 2^53, b > 0.  On the device a double-precision
+// estimate plus an exact integer correction (a 64-bit integer division is a
+// ~100-instruction subroutine; this runs in the kernel prologue).
+OWQ_HD int64_t fdiv(int64_t a, int64_t b) {
+#if defined(__CUDA_ARCH__)
+  int64_t q = (int64_t)((double)a / (double)b);
+  while (q * b > a) --q;
+  while ((q + 1) * b <= a) ++q;
+  return q;
+#else
+  return a / b;
+#endif
+}
+OWQ_HD int64_t cdiv(int64_t a, int64_t b) { return fdiv(a + b - 1, b); }
 OWQ_HD int words_per_row(int bits) { return bits == 3 ? 6 : 8; }
 
 struct Geo {
@@ -85,7 +98,7 @@ OWQ_HD int64_t item_offset(const Geo& g, int64_t rb, int32_t li) {   // relative
 // First item whose offset is >= b (b in [0, T]).
 OWQ_HD int64_t first_item_at(const Geo& g, int64_t b) {
   const int32_t n = items_per_rb(g);
-  int64_t rb = b / g.rb_bytes;
+  int64_t rb = fdiv(b, g.rb_bytes);
   int64_t r = b - rb * g.rb_bytes;
   if (rb >= g.nrb) return (int64_t)g.nrb * n;
   const int64_t C = (int64_t)g.nss * g.ss_bytes;
@@ -103,9 +116,9 @@ OWQ_HD int64_t cta_first_item(const Geo& g, int64_t grid, int64_t c) {
 
 OWQ_HD int64_t cta_of_item(const Geo& g, int64_t grid, int64_t item) {
   const int32_t n = items_per_rb(g);
-  const int64_t rb = item / n;
+  const int64_t rb = fdiv(item, n);
   const int64_t T = (int64_t)g.nrb * g.rb_bytes;
-  return item_offset(g, rb, (int32_t)(item - rb * n)) * grid / T;
+  return fdiv(item_offset(g, rb, (int32_t)(item - rb * n)) * grid, T);
 }
 
 // Stage sequence of one CTA: runs of at most `cap` items of one kind (code or
@@ -116,7 +129,7 @@ struct StageIter {
   int64_t left;
   OWQ_HD void init(const Geo& g, int64_t first, int64_t last, int32_t cap_) {
     n_rb = items_per_rb(g); nss = g.nss; cap = cap_;
-    rb = first / n_rb; li = (int32_t)(first - rb * n_rb); left = last - first;
+    rb = (int64_t)((uint32_t)first / (uint32_t)n_rb); li = (int32_t)(first - rb * n_rb); left = last - first;
   }
   // returns the number of items (0 = done); (srb, sli) = the stage's first item
   OWQ_HD int32_t next(int64_t& srb, int32_t& sli) {
