@@ -130,31 +130,39 @@ owq_status owq_blob_decode_host(const void *h_blob, size_t blob_bytes,
 owq_status owq_unpack_codes(const owq_shape *shape, const void *d_packed,
                             uint8_t *d_codes, void *stream);
 
-/* Workspace for the split-K (stream-K) reduction of owq_gemv /
- * owq_gemm_small_batch on the current device: per-row-block arrival counters
- * plus fp32 partial sums.  The caller zero-fills it ONCE; every call leaves
- * the counters at zero again.  One workspace must not be used by two calls
- * that may run concurrently. */
+/* Workspace of owq_gemv / owq_gemm_small_batch on the current device:
+ * per-row-block stream-K arrival counters, fp32 partial sums, and the exact
+ * int8 digit tiles + int64 digit sums of x written by each call's x pass.
+ * The caller zero-fills it ONCE; every call leaves the counters at zero again.
+ * One workspace must not be used by two calls that may run concurrently. */
 size_t owq_workspace_bytes(const owq_shape *shape, int batch);
 
 /* y = W_hat x for one activation vector (batch 1).
- * d_x: fp16 [c_in]; d_y: [c_out], fp32 if y_f32 else fp16 (RNE).
- * fp32 accumulation of exact (q - z) * x products. */
+ * d_x: fp16 [c_in] (finite values); d_y: [c_out], fp32 if y_f32 else fp16 (RNE).
+ * Arithmetic: x * 2^24 is split into 6 exact int8 digits, the
+ * codes are the u8 A operand of tcgen05.mma kind::i8 (s32 accumulate), and
+ * s * 2^-24 * (sum_i 256^i D_i - z * sum x 2^24) is formed exactly in fp64 then
+ * scaled in fp32; weak columns fp16 x fp16 in fp32.  Two launches on the
+ * stream (x digit pass + fused GEMV).  Errors: INVALID_ARG (NULL pointers),
+ * BAD_BLOB (header/shape mismatch), BUFFER_TOO_SMALL (workspace), CUDA. */
 owq_status owq_gemv(const owq_shape *shape, const void *d_packed,
                     const uint16_t *d_x, void *d_y, int y_f32,
                     void *d_workspace, size_t ws_bytes, void *stream);
 
 /* Y = W_hat X for B in [1, 16] activation rows: d_x fp16 [B][c_in] row-major,
- * d_y [B][c_out] (fp32 if y_f32).  Same arithmetic as owq_gemv; the tensor-core
- * B operand carries up to 8 activation rows per mma, 16 with two n-tiles. */
+ * d_y [B][c_out] (fp32 if y_f32).  Same arithmetic as owq_gemv; the MMA's N
+ * dimension carries the 6 digit rows of every activation row (N = 8 / 16 / 32
+ * / 64 / 96 for B = 1 / 2 / <= 5 / <= 10 / <= 16).  UNSUPPORTED if B is outside
+ * [1, 16]. */
 owq_status owq_gemm_small_batch(const owq_shape *shape, const void *d_packed,
                                 const uint16_t *d_x, int batch, void *d_y,
                                 int y_f32, void *d_workspace, size_t ws_bytes,
                                 void *stream);
 
 /* Test/tuning hook: same as owq_gemm_small_batch with an explicit grid size
- * (number of CTAs; 0 = one per SM).  Small grids exercise the stream-K
- * partial-sum path with many pieces per row-block. */
+ * (number of CTAs; 0 = one per SM; capped at one CTA per item; > 512 after the
+ * cap -> UNSUPPORTED).  Small grids exercise the stream-K partial-sum path with
+ * many pieces per row-block. */
 owq_status owq_gemm_small_batch_grid(const owq_shape *shape, const void *d_packed,
                                      const uint16_t *d_x, int batch, void *d_y,
                                      int y_f32, void *d_workspace, size_t ws_bytes,

@@ -1,0 +1,62 @@
+"""Write profiles/<round>_summary.md + profiles/ncu_traffic.json from the ncu
+artefacts of one round (launch list CSV + --set full reports of the GEMV on the
+two OPT-175B layer shapes).  python tools/profile_summary.py r1"""
+import csv, io, json, os, subprocess, sys
+from collections import defaultdict
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
+P = os.path.join(ROOT, "profiles")
+out = [f"# ncu summary, round {rnd[1:]}\n"]
+
+rows = list(csv.reader(open(os.path.join(P, f"{rnd}_bench_launches.csv"))))
+h = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+hdr = rows[h]; iK = hdr.index("Kernel Name"); iV = hdr.index("Metric Value")
+d = defaultdict(list)
+for r in rows[h + 1:]:
+    if len(r) == len(hdr):
+        d[r[iK].split("(")[0]].append(float(r[iV].replace(",", "")))
+tot = sum(sum(v) for v in d.values())
+out.append("## Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of "
+           "`bench.py --steps 2 --warmup 3 --no-graph` (cold, serialised launches)\n")
+out.append("| kernel | launches | median us | share of GPU time |\n|---|---|---|---|")
+for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
+    out.append(f"| `{k}` | {len(v)} | {sorted(v)[len(v) // 2] / 1e3:.2f} | {sum(v) / tot * 100:.1f}% |")
+
+def raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(txt)))
+    h = rr[0]
+    for r in rr[2:]:
+        if "owq_gemv_kernel" in "".join(r):
+            def g(n):
+                try: return float(r[h.index(n)].replace(",", ""))
+                except Exception: return float("nan")
+            return g
+    return None
+
+traffic = {}
+out.append("\n## `ncu --set full` of one owq_gemv_kernel launch (B = 1)\n")
+out.append("| shape | duration us | DRAM read MB | DRAM write MB | algorithmic MB | ALU pipe % | FMA pipe % | issue slots busy % |")
+out.append("|---|---|---|---|---|---|---|---|")
+for tag, (M, K, k) in {"q": (12288, 12288, 15), "fc1": (49152, 12288, 3), "fc2": (12288, 49152, 15)}.items():
+    rep = os.path.join(ROOT, "gpurun_out", f"prof_{rnd}_{tag}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
+    g = raw(rep)
+    alg = 3 * M * K / 8 + 4 * M + 2 * M * k + 2 * k + 2 * K + 2 * M
+    rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
+    unit = 1.0
+    traffic[tag] = {"dram_read_bytes": rd * 1e6, "dram_write_bytes": wr * 1e6, "algorithmic_bytes": alg,
+                    "duration_us": g("gpu__time_duration.sum") / 1e3 if g("gpu__time_duration.sum") > 1000 else g("gpu__time_duration.sum")}
+    out.append(f"| {tag} {M}x{K} | {traffic[tag]['duration_us']:.2f} | {rd:.2f} | {wr:.2f} | {alg / 1e6:.2f} | "
+               f"{g('sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active'):.1f} | "
+               f"{g('sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active'):.1f} | "
+               f"{g('sm__issue_active.avg.pct_of_peak_sustained_active'):.1f} |")
+open(os.path.join(P, f"{rnd}_summary.md"), "w").write("\n".join(out) + "\n")
+if traffic:
+    layer_tags = ["q", "q", "q", "q", "fc1", "fc2" if "fc2" in traffic else "fc1"]
+    per = [traffic[t]["dram_read_bytes"] + traffic[t]["dram_write_bytes"] for t in layer_tags]
+    json.dump({"round": rnd, "per_shape": traffic, "bytes_per_step": sum(per),
+               "note": "dram__bytes_read.sum + dram__bytes_write.sum of one --set full capture per shape; "
+                       "q/k/v/out share the q capture"}, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
+print("\n".join(out))
