@@ -29,7 +29,7 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libowq.so")
+LIB_PATH = os.environ.get("OWQ_LIB") or os.path.join(HERE, "libowq.so")   # OWQ_LIB: A/B experiments only
 
 OWQ_TP_ROWS, OWQ_TP_COLS = 0, 1
 OWQ_PACK_STRICT, OWQ_PACK_U8_CODES = 1, 2

@@ -47,7 +47,13 @@ def needs_build(force=False):
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, csrc: str = None, out: str = None, inc: str = None) -> str:
+    """csrc/out/inc: experiments only (A/B builds of another source tree into another file)."""
+    global CSRC, OUT, BUILD, INC
+    if csrc or out or inc:
+        CSRC, OUT, INC = csrc or CSRC, out or OUT, inc or INC
+        BUILD = OUT + "_build"
+        force = True
     if not needs_build(force):
         return OUT
     os.makedirs(BUILD, exist_ok=True)
@@ -75,4 +81,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    a = sys.argv
+    opt = lambda k: a[a.index(k) + 1] if k in a else None
+    print(build(force="--force" in a, verbose="-v" in a, csrc=opt("--csrc"), out=opt("--out"), inc=opt("--inc")))

@@ -78,6 +78,7 @@ struct Params {
   int64_t xK;             // row stride of x in elements
   int32_t group_log2;     // log2(group_size / 64)
   int32_t span[kMaxGrid + 1];  // first item of each CTA (stream-K split, host-computed)
+  int32_t coresident;          // grid <= SM count: fixed summer per row-block (see the fixup)
   unsigned long long* trace;   // experiments only (OWQ_TRACE)
   int32_t exp;                 // experiments only (OWQ_EXP): 3 = skip the TMEM stores
 };
@@ -99,6 +100,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
       "@!P bra WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Off-critical-path wait: the thread may be suspended (time hint) instead of
+// spinning, so long waits do not take issue slots from the decode/MMA warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, 0x989680;\n\t"
+      "@!P bra WAITS_%=;\n}" ::"r"(smem_addr(bar)),
       "r"(parity)
       : "memory");
 }
@@ -147,6 +159,12 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+
+// Programmatic dependent launch (the kernels are launched with programmatic
+// stream serialization): wait = all prerequisite grids completed and their
+// memory visible; launch_dependents = the next kernel in the stream may start.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // tcgen05 (5th-gen tensor core + TMEM)
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -287,6 +305,8 @@ __device__ __forceinline__ long long x_fixed(__half h) { return (long long)(__ha
 __global__ void owq_x_digits_kernel(const __half* __restrict__ x, int64_t xK, int B, int Bp, int K, int NN,
                                     uint8_t* __restrict__ tiles, long long* __restrict__ sums) {
   __shared__ long long part[2 * OWQ_MAX_BATCH];
+  pdl_wait();                  // x and the workspace belong to earlier kernels until they complete
+  pdl_launch_dependents();     // the GEMV may start its prologue and weight prefetch now
   const int ss = blockIdx.x;
   const int b = threadIdx.x >> 6, k = threadIdx.x & 63;   // blockDim = 64 * Bp
   const int nbk = NN / 8;
@@ -376,8 +396,8 @@ struct Cfg {
   static constexpr int kDCol0 = DWG * 2 * kABuf;          // A: [DWG][2] buffers, then D: [DWG][2] x NN columns
   static_assert(kDCol0 + DWG * 2 * NN <= kTmemCols, "TMEM budget");
   static_assert(kMaxB * kDigits <= NN, "digit rows");
-  // per stage: decode + epilogue warps arrive, each MMA warp commits (B is read from the stage)
-  static constexpr int kEmptyCount = kDecodeWarps + 4 + DWG;
+  // per stage: decode warps arrive, each MMA warp commits (B is read from the stage)
+  static constexpr int kEmptyCount = kDecodeWarps + DWG;
 };
 
 // Stage descriptor, written by the producer into shared memory before it
@@ -448,7 +468,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
   uint64_t* aempty = afull + DWG * 2;  // [DWG][2]  MMA done reading it
   uint64_t* dfull = aempty + DWG * 2;  // [DWG][2]  group accumulator complete
   uint64_t* dempty = dfull + 2 * DWG;  // [DWG][2]  epilogue drained it
-  uint64_t* tready = dempty + 2 * DWG;  // [NST]  digit tiles of the stage written (in-kernel digit mode, 4 warps)
+  uint64_t* tready = dempty + 2 * DWG;  // [NST]  digit tiles of the stage landed (TMA tx); only the MMA waits on it
   StageDesc* desc = reinterpret_cast<StageDesc*>(tready + NST);       // [NST]
   uint4* mbox = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(desc + NST) + 15) & ~(uintptr_t)15);   // [DWG][2] decode -> MMA notes
   int64_t* span = reinterpret_cast<int64_t*>(mbox + 2 * DWG);         // [2] this CTA's item range
@@ -460,7 +480,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
     if (p.trace) p.trace[cta * 256 + 0] = gtime();
     span[0] = p.span[cta];
     span[1] = p.span[cta + 1];
-    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); mbar_init(&tready[s], 4); }
+    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); mbar_init(&tready[s], 1); }
     for (int i = 0; i < 2 * DWG; ++i) {
       mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4);
     }
@@ -482,30 +502,61 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
   if (warp == C::kProdWarp) {
     // ==================================================================== producer
     if (lane == 0) {
+      pdl_launch_dependents();
       const uint64_t pol = evict_first_policy(), pol_x = evict_last_policy();
+      // Until the x-digit pass (the previous kernel) has completed, only the
+      // weight codes are prefetched; the digit-tile copies of those stages are
+      // issued after pdl_wait().
+      bool dep = false;
+      int npend = 0;
+      int32_t pend_sli[8], pend_n[8], pend_s[8];
+      auto resolve = [&]() {
+        pdl_wait();
+        dep = true;
+        for (int i = 0; i < npend; ++i)
+          bulk_g2s(ring + (size_t)pend_s[i] * p.stage_bytes + p.tile_off, p.tiles + (int64_t)pend_sli[i] * tile_bytes,
+                   (uint32_t)pend_n[i] * tile_bytes, &tready[pend_s[i]], pol_x);
+        npend = 0;
+      };
+      // code stages only: weak chunks never enter the ring (the epilogue reads them)
       StageIter it;
       it.init(g, i0, i1, p.cap);
+      auto next_code = [&](int64_t& rb_, int32_t& li_) {
+        int32_t m;
+        while ((m = it.next(rb_, li_)) > 0 && li_ >= g.nss) {}
+        return m;
+      };
       int64_t srb, nrb = 0;
       int32_t sli, nli = 0;
-      int32_t n = it.next(srb, sli);
+      int32_t n = next_code(srb, sli);
       int s = 0, k = 0;
       uint32_t ph = 0;
       while (n > 0) {
-        const int32_t nn = it.next(nrb, nli);
-        if (k >= NST) mbar_wait(&empty[s], ph ^ 1u);
+        const int32_t nn = next_code(nrb, nli);
+        if (k >= NST) {
+          if (!dep) resolve();
+          mbar_wait(&empty[s], ph ^ 1u);
+        }
         if (p.trace && k < 32) p.trace[cta * 256 + 64 + k] = gtime();
-        const bool code = sli < g.nss;
+        const bool code = true;
         uint32_t fl = 0;
         if (nn == 0 || nrb != srb) fl |= kRbEnd;
-        else if (code && nli < g.nss && group_of(p, nli) == group_of(p, sli + n - 1)) fl |= kGroupCont;
+        else if (group_of(p, nli) == group_of(p, sli + n - 1)) fl |= kGroupCont;
         asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(smem_addr(&desc[s])), "r"((uint32_t)srb),
                      "r"((uint32_t)(sli & 0xFFFF) | ((uint32_t)n << 16) | (fl << 24)) : "memory");
         uint8_t* st = ring + (size_t)s * p.stage_bytes;
         const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
         if (code && !C::kInDig) {
-          mbar_expect_tx(&full[s], cbytes + (uint32_t)n * tile_bytes);
+          // codes -> full[s] (decode), digit tiles -> tready[s] (MMA only), so the
+          // decode can run while the x-digit pass is still producing the tiles
+          mbar_expect_tx(&full[s], cbytes);
+          mbar_expect_tx(&tready[s], (uint32_t)n * tile_bytes);
           bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
-          bulk_g2s(st + p.tile_off, p.tiles + (int64_t)sli * tile_bytes, (uint32_t)n * tile_bytes, &full[s], pol_x);
+          if (dep) {
+            bulk_g2s(st + p.tile_off, p.tiles + (int64_t)sli * tile_bytes, (uint32_t)n * tile_bytes, &tready[s], pol_x);
+          } else {
+            pend_sli[npend] = sli; pend_n[npend] = n; pend_s[npend] = s; ++npend;
+          }
         } else if (code) {
           // codes + the x columns of the stage (x rows are 16-byte aligned, K % 8 == 0: host-checked)
           const int64_t col0 = (int64_t)sli * kSuperStep;
@@ -524,6 +575,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
         sli = nli;
         n = nn;
       }
+      if (!dep) resolve();
       // terminal descriptor: consumers leave their loops
       if (k >= NST) mbar_wait(&empty[s], ph ^ 1u);
       asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(smem_addr(&desc[s])), "r"(0u) : "memory");
@@ -568,8 +620,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
           const uint32_t a_lo = sbase + (uint32_t)lo * kSS + (uint32_t)row * 16u;
           const uint32_t a_hi = sbase + (uint32_t)lo * kSS + 2048u + (uint32_t)row * kHiStride;
           const uint32_t tcol = trow + buf * (uint32_t)C::kABuf;
-          auto item = [&](int t) {
-            uint32_t w[8];
+          auto load_item = [&](int t, uint32_t* w) {
             const uint4 a = lds128(a_lo + t * kSS);
             w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
             if (BITS == 3) {
@@ -579,6 +630,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
               const uint4 b = lds128(a_hi + t * kSS);
               w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
             }
+          };
+          auto store_item = [&](int t, const uint32_t* w) {
             uint32_t o[16];
             decode_row<BITS>(w, o, sh);
             tc_st16(tcol + t * C::kACols, o);
@@ -586,9 +639,17 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
           if (p.exp == 3) {
           } else if (hi - lo == C::kIPW) {   // full share: unrolled, immediate offsets
 #pragma unroll
-            for (int t = 0; t < C::kIPW; ++t) item(t);
+            for (int t = 0; t < C::kIPW; ++t) {
+              uint32_t w[8];
+              load_item(t, w);
+              store_item(t, w);
+            }
           } else {
-            for (int t = 0; t < hi - lo; ++t) item(t);
+            for (int t = 0; t < hi - lo; ++t) {
+              uint32_t w[8];
+              load_item(t, w);
+              store_item(t, w);
+            }
           }
           if (C::kInDig) {
             // digit tiles of this warpgroup's items: warp q converts items lo+q, lo+q+4, ..
@@ -631,8 +692,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[wg * 2 + buf]);
         if (d.n == 0) break;
-      } else if (q == 0 && lane == 0) {
-        mbar_arrive(&empty[s]);   // weak stage: on behalf of this warpgroup's MMA warp, which never sees it
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -650,7 +709,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
     constexpr uint32_t kLbo = (NN / 8) * 128;          // K-adjacent core matrices
     const uint32_t ring0 = smem_addr(ring) + (uint32_t)p.tile_off;
     int kst = 0;
-    long long c_wait = 0, c_issue = 0, c_commit = 0, c_mma = 0;   // trace only
+    long long c_wait = 0, c_issue = 0, c_commit = 0, c_mma = 0, c_tready = 0, c_dempty = 0;   // trace only
     for (;;) {
       const uint32_t buf = acnt & 1u;
       const long long t0 = clock64();
@@ -666,13 +725,18 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
       d.flags = (uint8_t)(note.z >> 24);
       d.rb = (int32_t)note.w;
       const int s = (int)(note.x & 0x7FFFFFFFu), lo = (int)((note.z >> 8) & 0xFF), hi = (int)((note.z >> 16) & 0xFF);
+      const long long tt0 = clock64();
+      if (!C::kInDig) mbar_wait(&tready[s], note.x >> 31);   // this stage's digit tiles
+      c_tready += clock64() - tt0;
       if (p.trace && wg == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
       tc_fence_after();
       const uint32_t stile = ring0 + (uint32_t)s * (uint32_t)p.stage_bytes;
       if (!p.g.group && hi - lo == C::kIPW) {
         // common case: one scale group, full share -> one asm block, one elect
         const uint32_t dbuf = dcnt & 1u;
+        const long long td0 = clock64();
         if (!open && dcnt >= 2) mbar_wait(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
+        c_dempty += clock64() - td0;
         tc_mma_i8_stage<C::kIPW, NN * kSuperStep, kLbo>(
             tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * NN), a_wg + buf * (uint32_t)C::kABuf,
             umma_desc(stile + (uint32_t)lo * tile_bytes, kLbo, 128), idesc_i8<NN>(), open ? 1u : 0u);
@@ -721,9 +785,16 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
       p.trace[cta * 256 + 5 + wg] = (unsigned long long)c_issue;
       p.trace[cta * 256 + 9 + wg * 0] = (unsigned long long)c_commit;
       p.trace[cta * 256 + 52] = (unsigned long long)c_mma;
+      p.trace[cta * 256 + 42 + wg] = (unsigned long long)c_tready;
+      p.trace[cta * 256 + 46 + wg] = (unsigned long long)c_dempty;
     }
   } else {
     // ==================================================================== epilogue
+    // Independent of the shared-memory ring: walks this CTA's item sequence
+    // itself (the producer's stage partition, without waiting on stages),
+    // prefetches each scale group's scale/zero, digit sums and the row's weak
+    // values from global memory when the group opens, and only waits on the
+    // D accumulators (dfull) at the group end.
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int et = threadIdx.x - C::kEpiWarp0 * 32;     // 0..127
@@ -734,108 +805,94 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
         xw[i] = t < g.k ? p.x[(int64_t)b * p.xK + widx[t]] : __float2half(0.f);
       }
     }
+    pdl_wait();   // digit sums (p.sums) come from the x-digit pass
     named_sync(2, 128);
     constexpr double kPow256[6] = {1.0, 256.0, 65536.0, 16777216.0, 4294967296.0, 1099511627776.0};
+    const int gl = g.group ? p.group_log2 : 30;
     float tot[MAXB];
-    long long sgrp[MAXB];                                // in-kernel digit mode: sum of the open group's digit sums
+    long long sacc[MAXB];                                // this thread's share of the open group's digit sums
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b) { tot[b] = 0.f; sgrp[b] = 0; }
+    for (int b = 0; b < MAXB; ++b) { tot[b] = 0.f; sacc[b] = 0; }
     uint32_t dcnt[DWG];
 #pragma unroll
     for (int w = 0; w < DWG; ++w) dcnt[w] = 0;
     uint32_t part = 0;                                   // warpgroups with items in the open group
-    int gfirst = -1;                                     // first item (li) of the open group in this CTA
-    int kst = 0, rr = 0;
-    int s = 0;
-    uint32_t ph = 0;
-    for (;;) {
-      if (q == 0) mbar_wait(&full[s], ph);
-      named_sync(2, 128);
-      const StageDesc d = load_desc(&desc[s]);
-      if (d.n == 0) break;
-      const bool code = d.li < g.nss;
-      const uint32_t sbase_e = smem_addr(ring + (size_t)s * p.stage_bytes);
-      (void)sbase_e;
-      if (code) {
-        long long sst[MAXB];   // this stage's digit sums of the items of each segment (in-kernel digit mode)
-        if (!C::kInDig) {
-          // nothing in a code stage's shared memory is needed here: release it now
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
-        }
-        for (int pa = 0; pa < d.n;) {
-          const Seg sg = segment(p, pa, d);
-          if (gfirst < 0) gfirst = d.li + sg.pa;
-          if (d.n == p.cap && !p.g.group) {
+    bool gopen = false;
+    uint32_t szw = 0;                                    // the open group's (s, z) for this row
+    uint4 wpre[2];                                       // this row's first two weak chunks of the row-block (prefetch)
+    int64_t wpre_rb = -1;
+    int ngend = 0, kst = 0, rr = 0;
+    StageIter it;
+    it.init(g, i0, i1, p.cap);
+    int64_t crb, nrb = -1;
+    int32_t cli, nli = 0;
+    int32_t cn = it.next(crb, cli);
+    while (cn > 0) {
+      const int32_t nn = it.next(nrb, nli);
+      if (cli < g.nss) {
+        for (int pa = 0; pa < cn;) {
+          const int gi = (cli + pa) >> gl;
+          const int gend = ((gi + 1) << gl) - cli - 1;   // last stage position of this group
+          const int pb = gend < cn - 1 ? gend : cn - 1;
+          const bool ends = pb + 1 < cn || !(nn > 0 && nrb == crb && nli < g.nss && (nli >> gl) == gi);
+          if (wpre_rb != crb) {
+            // row-block opens: prefetch this row's weak values of the CTA's first two
+            // weak chunks of the row-block (full chunks only; the rest load on demand)
+            wpre_rb = crb;
+            const int64_t w0 = (i0 > crb * n_rb + g.nss ? i0 - crb * n_rb : g.nss) - g.nss;   // first weak chunk in this CTA
+            const int64_t w1 = (i1 < (crb + 1) * n_rb ? i1 - crb * n_rb : n_rb) - g.nss;
+            const uint8_t* wb = p.blob + g.units_off + item_offset(g, crb, g.nss);
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              wpre[j] = make_uint4(0, 0, 0, 0);
+              if (w0 + j < w1 && w0 + j < g.nfull)
+                wpre[j] = __ldg(reinterpret_cast<const uint4*>(wb + (w0 + j) * kWeakChunkBytes + row * 16));
+            }
+          }
+          if (!gopen) {
+            // group opens: prefetch (s, z) of this row and this thread's share of the
+            // group's digit sums (items gfirst .. glast of this CTA)
+            gopen = true;
+            szw = __ldg(reinterpret_cast<const unsigned int*>(p.blob + g.sz_off + ((int64_t)crb * g.G + gi) * kSZBlockBytes +
+                                                              row * 4));
+            const int gfirst = cli + pa;
+            const int64_t cend = (i1 - crb * n_rb < (int64_t)g.nss ? i1 - crb * n_rb : (int64_t)g.nss) - 1;   // CTA's last code item in rb
+            const int glast = (int)(((int64_t)((gi + 1) << gl) - 1 < cend) ? ((gi + 1) << gl) - 1 : cend);
+            for (int li = gfirst + et; li <= glast; li += 128)
+#pragma unroll
+              for (int b = 0; b < MAXB; ++b)
+                if (b < p.B) sacc[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
+          }
+          if (cn == p.cap && !g.group) {
             part = (1u << DWG) - 1u;   // full stage, one segment: every warpgroup has items
           } else {
 #pragma unroll
             for (int w = 0; w < DWG; ++w) {
               int lo, hi;
-              share<DWG>(d.n, w, lo, hi);
-              if (lo <= sg.pb && hi > sg.pa) part |= 1u << w;
+              share<DWG>(cn, w, lo, hi);
+              if (lo <= pb && hi > pa) part |= 1u << w;
             }
           }
-          if (C::kInDig) {
-            // this thread's share of sum x * 2^24 over the segment's columns (raw x in the stage)
-            const int ncol = (sg.pb - sg.pa + 1) * kSuperStep;
-            const int64_t cbase = (int64_t)(d.li + sg.pa) * kSuperStep;
+          if (ends) {
+            if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 18 + 6 * ngend] = gtime();
+            // block-reduce the digit-sum shares (the same for every row)
+            long long S[MAXB];
+            long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
+#pragma unroll
+            for (int b = 0; b < MAXB; ++b) {
+              long long v = sacc[b];
+              sacc[b] = 0;
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+              if (lane == 0) rd[q * OWQ_MAX_BATCH + b] = v;
+            }
+            named_sync(2, 128);
 #pragma unroll
             for (int b = 0; b < MAXB; ++b)
-              if (b < p.B)
-                for (int c = et; c < ncol; c += 128) {
-                  const __half h = __ushort_as_half((unsigned short)(lds32(sbase_e + (uint32_t)p.x_off +
-                      (uint32_t)(b * p.cap * kSuperStep + sg.pa * kSuperStep + (c & ~1)) * 2u) >> (16 * (c & 1))));
-                  if (cbase + c < g.K) sgrp[b] += x_fixed(h);
-                }
-          }
-          if (sg.ends) {
-            // x * 2^24 summed over the group's items (exact)
-            const int glast = d.li + sg.pb, cnt = glast - gfirst + 1;
-            long long S[MAXB];
-#pragma unroll
-            for (int b = 0; b < MAXB; ++b) S[b] = 0;
-            if (C::kInDig) {
-              // block-reduce the threads' shares (the same for every row)
-              long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
-#pragma unroll
-              for (int b = 0; b < MAXB; ++b) {
-                long long v = sgrp[b];
-                sgrp[b] = 0;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0) rd[q * OWQ_MAX_BATCH + b] = v;
-              }
-              named_sync(2, 128);
-#pragma unroll
-              for (int b = 0; b < MAXB; ++b)
-                S[b] = rd[b] + rd[OWQ_MAX_BATCH + b] + rd[2 * OWQ_MAX_BATCH + b] + rd[3 * OWQ_MAX_BATCH + b];
-              ++rr;
-            } else if (cnt <= 8) {
-              for (int li = gfirst; li <= glast; ++li)
-#pragma unroll
-                for (int b = 0; b < MAXB; ++b)
-                  if (b < p.B) S[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
-            } else {
-              for (int li = gfirst + et; li <= glast; li += 128)
-#pragma unroll
-                for (int b = 0; b < MAXB; ++b)
-                  if (b < p.B) S[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
-              long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
-#pragma unroll
-              for (int b = 0; b < MAXB; ++b) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) S[b] += __shfl_xor_sync(0xffffffffu, S[b], o);
-                if (lane == 0) rd[q * OWQ_MAX_BATCH + b] = S[b];
-              }
-              named_sync(2, 128);
-#pragma unroll
-              for (int b = 0; b < MAXB; ++b)
-                S[b] = rd[b] + rd[OWQ_MAX_BATCH + b] + rd[2 * OWQ_MAX_BATCH + b] + rd[3 * OWQ_MAX_BATCH + b];
-              ++rr;
-            }
-            const __half2 szv = u2h(__ldg(reinterpret_cast<const unsigned int*>(
-                p.blob + g.sz_off + ((int64_t)d.rb * g.G + sg.gi) * kSZBlockBytes + row * 4)));
+              S[b] = rd[b] + rd[OWQ_MAX_BATCH + b] + rd[2 * OWQ_MAX_BATCH + b] + rd[3 * OWQ_MAX_BATCH + b];
+            ++rr;
+            if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 19 + 6 * ngend] = gtime();
+            const __half2 szv = u2h(szw);
             const float s_g = __low2float(szv);
             const double z_g = (double)__high2float(szv);
             double dacc[MAXB];
@@ -845,7 +902,9 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
             for (int w = 0; w < DWG; ++w) {
               if (part & (1u << w)) {   // fixed order over warpgroups: deterministic
                 const uint32_t dbuf = dcnt[w] & 1u;
-                mbar_wait(&dfull[w * 2 + dbuf], (dcnt[w] >> 1) & 1u);
+                // one warp waits (suspending), the others block on the named barrier
+                if (q == 0) mbar_wait(&dfull[w * 2 + dbuf], (dcnt[w] >> 1) & 1u);
+                named_sync(2, 128);
                 tc_fence_after();
                 const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * NN);
 #pragma unroll
@@ -864,27 +923,30 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
                 ++dcnt[w];
               }
             }
+            if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 20 + 6 * ngend] = gtime();
 #pragma unroll
             for (int b = 0; b < MAXB; ++b)
               tot[b] = fmaf(s_g, (float)((dacc[b] - z_g * (double)S[b]) * 5.9604644775390625e-08), tot[b]);
+            if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 21 + 6 * ngend] = gtime();
+            ++ngend;
             part = 0;
-            gfirst = -1;
+            gopen = false;
           }
-          pa = sg.pb + 1;
+          pa = pb + 1;
         }
-        if (C::kInDig) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[s]);
-        }
-        (void)sst;
       } else {
-        // weak chunks: fp16 weak columns x gathered activations, fp32 (unscaled)
-        const uint32_t sbase = smem_addr(ring + (size_t)s * p.stage_bytes);
-        for (int pi = 0; pi < d.n; ++pi) {
-          const int gch = d.li - g.nss + pi;
+        // weak chunks (straight from the blob, not through the ring): fp16 weak
+        // columns x gathered activations, fp32 (unscaled)
+        const uint8_t* wbase = p.blob + g.units_off + item_offset(g, crb, cli);
+        for (int pi = 0; pi < cn; ++pi) {
+          const int gch = cli - g.nss + pi;
           float v[8];
           if (gch < g.nfull) {
-            const uint4 a = lds128(sbase + pi * kWeakChunkBytes + row * 16);
+            const int64_t w0 = (i0 > crb * n_rb + g.nss ? i0 - crb * n_rb : g.nss) - g.nss;
+            const int jpre = (int)(gch - w0);
+            const uint4 a = (wpre_rb == crb && jpre >= 0 && jpre < 2)
+                                ? (jpre == 0 ? wpre[0] : wpre[1])
+                                : __ldg(reinterpret_cast<const uint4*>(wbase + (size_t)pi * kWeakChunkBytes + row * 16));
             const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
@@ -893,7 +955,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
               v[2 * c + 1] = f.y;
             }
           } else {
-            const __half* tl = reinterpret_cast<const __half*>(ring + (size_t)s * p.stage_bytes + (size_t)pi * kWeakChunkBytes);
+            const __half* tl = reinterpret_cast<const __half*>(wbase + (size_t)pi * kWeakChunkBytes);
 #pragma unroll
             for (int c = 0; c < 8; ++c) v[c] = c < g.ktail ? __half2float(tl[row * g.ktail + c]) : 0.f;
           }
@@ -913,17 +975,13 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
       }
       if (p.trace && et == 0 && kst < 32) p.trace[cta * 256 + 160 + kst] = gtime();
       ++kst;
-      if (++s == NST) { s = 0; ph ^= 1u; }
 
-      if (d.flags & kRbEnd) {
-        // -------------------------------------------------- finish row-block d.rb
+      if (nn == 0 || nrb != crb) {
+        // -------------------------------------------------- finish row-block crb
         if (p.trace && et == 0) p.trace[cta * 256 + 50] = gtime();
-        const int64_t crb = d.rb;
         const int64_t ifirst = crb * n_rb, ilast = ifirst + n_rb - 1;
         const bool whole = ifirst >= i0 && ilast < i1;
         const int64_t grow = crb * kRowBlock + row;
@@ -953,7 +1011,27 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
           const int64_t c_first = cta_of(ifirst), c_last = cta_of(ilast);
           const int npieces = (int)(c_last - c_first + 1);
           named_sync(2, 128);
-          if (et == 0) {
+          if (p.coresident && cta != c_first) {
+            // Fixed summer = the CTA holding the row-block's first item (it reaches
+            // the row-block last).  Other pieces publish with a release add (only
+            // that thread waits for its release fence) and go on; the summer
+            // acquires the count, then sums all pieces in a fixed order.
+            if (et == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + crb) : "memory");
+          } else {
+          if (p.coresident) {
+            {
+              if (et == 0) {
+                unsigned c;
+                for (;;) {
+                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(p.counters + crb) : "memory");
+                  if (c == (unsigned)(npieces - 1)) break;
+                  __nanosleep(200);
+                }
+                p.counters[crb] = 0u;   // reset for the next call
+              }
+              *flag = 1;
+            }
+          } else if (et == 0) {
             // acq_rel: releases this CTA's partial stores (ordered before by the
             // barrier), acquires the other pieces' stores when we are last
             unsigned old;
@@ -973,11 +1051,15 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
             }
           }
           named_sync(2, 128);
+          }
         }
 #pragma unroll
         for (int b = 0; b < MAXB; ++b) tot[b] = 0.f;
         if (p.trace && et == 0) p.trace[cta * 256 + 56] = gtime();
       }
+      crb = nrb;
+      cli = nli;
+      cn = nn;
     }
   }
   // teardown: every role is done with TMEM
@@ -1115,7 +1197,18 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
       return OWQ_ERR_CUDA;
     configured = smem;
   }
-  kern<<<(unsigned)grid, C::kThreads, smem, stream>>>(p);
+  static const int pdl = getenv("OWQ_PDL") ? atoi(getenv("OWQ_PDL")) : 2;   // experiments: 0 off, 1 GEMV, 2 both
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl >= 1 ? 1 : 0;
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, p);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "owq: launch of owq_gemv_kernel<%d,%d,%d> (grid %lld, smem %zu) failed: %s\n", BITS, NN, DWG,
@@ -1129,10 +1222,10 @@ template <int BITS>
 static owq_status launch_n(const Params& p, int64_t grid, cudaStream_t cs) {
   static const int dwg = getenv("OWQ_DWG") ? atoi(getenv("OWQ_DWG")) : 0;   // experiments (B = 1 only)
   switch (mma_n_for(p.B)) {
-    case 8:
-      if (dwg == 2) return launch<BITS, 8, 2>(p, grid, cs);
+    case 8:   // batch 1: 2 decode warpgroups x 6 items measured best (fewer TMEM stores racing the MMAs)
+      if (dwg == 3) return launch<BITS, 8, 3>(p, grid, cs);
       if (dwg == 4) return launch<BITS, 8, 4>(p, grid, cs);
-      return launch<BITS, 8, 3>(p, grid, cs);
+      return launch<BITS, 8, 2>(p, grid, cs);
     case 16: return launch<BITS, 16, 4>(p, grid, cs);
     case 32: return launch<BITS, 32, 4>(p, grid, cs);
     case 64: return launch<BITS, 64, 2>(p, grid, cs);
@@ -1162,6 +1255,7 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.sums = sums;
   p.g = g;
   for (int64_t c = 0; c <= grid; ++c) p.span[c] = (int32_t)cta_first_item(g, grid, c);
+  p.coresident = grid <= device_sms() ? 1 : 0;   // one CTA per SM: every CTA is resident at once
   p.B = B;
   p.Bp = batch_pad(B);
   p.y_f32 = y_f32 ? 1 : 0;
@@ -1178,8 +1272,20 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
     p.xK = Kp;
   }
   // x -> exact int8 digits in UMMA tile order, plus per-super-step digit sums
-  {
-    owq_x_digits_kernel<<<(unsigned)g.nss, 64 * p.Bp, 0, cs>>>(p.x, p.xK, B, p.Bp, g.K, mma_n_for(B), tiles, sums);
+  static const int skip = getenv("OWQ_SKIP") ? atoi(getenv("OWQ_SKIP")) : 0;   // experiments: 1 no digit pass, 2 no GEMV
+  if (skip != 1) {
+    static const int pdl = getenv("OWQ_PDL") ? atoi(getenv("OWQ_PDL")) : 2;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl >= 2 ? 1 : 0;
+    cfg.gridDim = dim3((unsigned)g.nss);
+    cfg.blockDim = dim3((unsigned)(64 * p.Bp));
+    cfg.stream = cs;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, owq_x_digits_kernel, (const __half*)p.x, (int64_t)p.xK, B, (int)p.Bp, (int)g.K,
+                       mma_n_for(B), tiles, (long long*)sums);
     if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
   }
   static unsigned long long* trace_buf = nullptr;
@@ -1191,7 +1297,7 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.exp = exp_env;
   p.group_log2 = 0;
   if (g.group) while ((kSuperStep << p.group_log2) < g.group) ++p.group_log2;
-  const owq_status rs = g.bits == 3 ? launch_n<3>(p, grid, cs) : launch_n<4>(p, grid, cs);
+  const owq_status rs = skip == 2 ? OWQ_OK : (g.bits == 3 ? launch_n<3>(p, grid, cs) : launch_n<4>(p, grid, cs));
   if (trace_buf && rs == OWQ_OK) {   // experiments only: dump the per-CTA stamps
     std::vector<unsigned long long> h((size_t)grid * 256);
     cudaMemcpyAsync(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost, cs);

@@ -1,6 +1,6 @@
 #!/bin/bash
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -2
-for sk in 0 1; do
+for sk in 0 1 2; do
   echo -n "SKIP=$sk "; OWQ_SKIP=$sk timeout 120 python tools/prof_gemv.py 12288 12288 3 0 15 1 40
   echo -n "SKIP=$sk "; OWQ_SKIP=$sk timeout 120 python tools/prof_gemv.py 49152 12288 3 0 3 1 12
+  echo -n "SKIP=$sk "; OWQ_SKIP=$sk timeout 120 python tools/prof_gemv.py 4096 4096 3 0 5 1 40
 done

@@ -30,4 +30,16 @@ for kk in range(0, 16):
     print(f" {kk:5d} " + " ".join(vals))
 print(" MMA warps (cycles, mean over CTAs): wait afull", [int(t[:, 1 + w].mean()) for w in range(4)],
       " issue", [int(t[:, 5 + w].mean()) for w in range(4)], " commit(wg3)", int(t[:, 9].mean()), " MMAs(wg3)", int(t[:, 52].mean()))
+print(" MMA waits (cycles, mean): tready", [int(t[:, 42 + w].mean()) for w in range(4)], " dempty", [int(t[:, 46 + w].mean()) for w in range(4)])
 print(" kernel cycles ~", int((np.median(t[:, 62]) - np.median(t[:, 0])) * 1.9))
+order = np.argsort(-t[:, 62])
+print(" slowest CTAs: idx  start  fin-in  fin-out  end   (us)   last-stage epi_done")
+for c in order[:6]:
+    eds = [v for v in t[c, 160:192] if v > 0]
+    print(f"   {c:4d} {rel(t[c,0]):6.2f} {rel(t[c,50]):7.2f} {rel(t[c,56]):8.2f} {rel(t[c,62]):6.2f}    stages {len(eds)}  epi_done " +
+          " ".join(f"{rel(v):.2f}" for v in eds))
+print(" group ends of the slowest CTAs: [stage-seen, S done, sz done, D+combine done] (us)")
+for c in order[:4]:
+    print("   ", c, [[round(rel(t[c, 18 + 6 * j + i]), 2) for i in range(4)] for j in range(2) if t[c, 18 + 6 * j] > 0])
+med = [[float(np.median(rel(t[t[:, 18 + 6 * j] > 0, 18 + 6 * j + i]))) for i in range(4)] for j in range(2)]
+print(" median group-end timeline:", [[round(v, 2) for v in m] for m in med])
