@@ -305,8 +305,11 @@ __device__ __forceinline__ long long x_fixed(__half h) { return (long long)(__ha
 __global__ void owq_x_digits_kernel(const __half* __restrict__ x, int64_t xK, int B, int Bp, int K, int NN,
                                     uint8_t* __restrict__ tiles, long long* __restrict__ sums) {
   __shared__ long long part[2 * OWQ_MAX_BATCH];
+  // Let the GEMV start (prologue, weight prefetch, decode) as soon as SMs free up,
+  // even before the previous GEMV has finished; everything it reads that depends on
+  // earlier kernels (x, digit tiles / sums, workspace) is behind its own pdl_wait().
+  pdl_launch_dependents();
   pdl_wait();                  // x and the workspace belong to earlier kernels until they complete
-  pdl_launch_dependents();     // the GEMV may start its prologue and weight prefetch now
   const int ss = blockIdx.x;
   const int b = threadIdx.x >> 6, k = threadIdx.x & 63;   // blockDim = 64 * Bp
   const int nbk = NN / 8;
@@ -798,6 +801,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int et = threadIdx.x - C::kEpiWarp0 * 32;     // 0..127
+    pdl_wait();   // x may come from the previous kernels; digit sums (p.sums) from the x-digit pass
     {  // x gathered at the weak columns, x[b][idx[t]] (0 for padding)
       const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
       for (int i = et; i < p.B * g.kpad; i += 128) {
@@ -805,7 +809,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
         xw[i] = t < g.k ? p.x[(int64_t)b * p.xK + widx[t]] : __float2half(0.f);
       }
     }
-    pdl_wait();   // digit sums (p.sums) come from the x-digit pass
     named_sync(2, 128);
     constexpr double kPow256[6] = {1.0, 256.0, 65536.0, 16777216.0, 4294967296.0, 1099511627776.0};
     const int gl = g.group ? p.group_log2 : 30;
@@ -822,6 +825,21 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
     uint4 wpre[2];                                       // this row's first two weak chunks of the row-block (prefetch)
     int64_t wpre_rb = -1;
     int ngend = 0, kst = 0, rr = 0;
+    auto cta_of = [&](int64_t item) {   // span table search: span[c] <= item < span[c + 1]
+      int lo_c = 0, hi_c = (int)grid;
+      while (hi_c - lo_c > 1) {
+        const int mid = (lo_c + hi_c) >> 1;
+        if (p.span[mid] <= item) lo_c = mid; else hi_c = mid;
+      }
+      return (int64_t)lo_c;
+    };
+    // Early fixup of the summer (co-resident grids, batch <= 2): the other pieces of
+    // a row-block stored their partials long before the summer reaches it, so the
+    // summer checks the count when it opens its last group of that row-block and,
+    // if complete, loads their partials then; at the finish it only adds them.
+    constexpr int kPreMax = 8;
+    float pre[MAXB <= 2 ? MAXB : 1][kPreMax];
+    int64_t pre_rb = -1;
     StageIter it;
     it.init(g, i0, i1, p.cap);
     int64_t crb, nrb = -1;
@@ -875,6 +893,32 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
           }
           if (ends) {
             if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 18 + 6 * ngend] = gtime();
+            // summer of a split row-block, last group: acquire the other pieces' count
+            // and load their partials now, while the pipeline drains this group
+            const int64_t cend_e = (i1 - crb * n_rb < (int64_t)g.nss ? i1 - crb * n_rb : (int64_t)g.nss) - 1;
+            if (MAXB <= 2 && p.coresident && cli + pb == cend_e && pre_rb != crb && crb * n_rb >= i0 &&
+                crb * n_rb + n_rb - 1 >= i1) {
+              const int64_t c_last = cta_of(crb * n_rb + n_rb - 1);
+              const int npieces = (int)(c_last - cta + 1);
+              if (npieces - 1 <= kPreMax) {
+                if (et == 0) {
+                  unsigned c;
+                  for (;;) {
+                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(p.counters + crb) : "memory");
+                    if (c == (unsigned)(npieces - 1)) break;
+                    __nanosleep(100);
+                  }
+                }
+                named_sync(2, 128);
+                pre_rb = crb;
+#pragma unroll
+                for (int b = 0; b < (MAXB <= 2 ? MAXB : 1); ++b)
+#pragma unroll
+                  for (int qq = 0; qq < kPreMax; ++qq)
+                    pre[b][qq] = (b < p.B && qq < npieces - 1)
+                                     ? __ldcg(&p.partial[((crb + cta + 1 + qq) * p.B + b) * kRowBlock + row]) : 0.f;
+              }
+            }
             // block-reduce the digit-sum shares (the same for every row)
             long long S[MAXB];
             long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
@@ -998,20 +1042,26 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
 #pragma unroll
           for (int b = 0; b < MAXB; ++b)
             if (b < p.B) __stcg(&p.partial[((crb + cta) * p.B + b) * kRowBlock + row], tot[b]);
-          // pieces = CTAs cta_of(first item) .. cta_of(last item) (none is empty)
-          // pieces = CTAs holding the first .. last item of the row-block (span table search)
-          auto cta_of = [&](int64_t item) {
-            int lo_c = 0, hi_c = (int)grid;   // span[lo_c] <= item < span[hi_c]
-            while (hi_c - lo_c > 1) {
-              const int mid = (lo_c + hi_c) >> 1;
-              if (p.span[mid] <= item) lo_c = mid; else hi_c = mid;
-            }
-            return (int64_t)lo_c;
-          };
+          // pieces = CTAs holding the first .. last item of the row-block (none is empty)
           const int64_t c_first = cta_of(ifirst), c_last = cta_of(ilast);
           const int npieces = (int)(c_last - c_first + 1);
           named_sync(2, 128);
-          if (p.coresident && cta != c_first) {
+          if (MAXB <= 2 && pre_rb == crb) {
+            // summer with the other pieces prefetched: fixed-order sum, no round trip
+            if (et == 0) p.counters[crb] = 0u;
+            if (grow < g.M) {
+#pragma unroll
+              for (int b = 0; b < (MAXB <= 2 ? MAXB : 1); ++b)
+                if (b < p.B) {
+                  float v = tot[b];
+#pragma unroll
+                  for (int qq = 0; qq < kPreMax; ++qq)
+                    if (qq < npieces - 1) v += pre[b][qq];
+                  if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = v;
+                  else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(v);
+                }
+            }
+          } else if (p.coresident && cta != c_first) {
             // Fixed summer = the CTA holding the row-block's first item (it reaches
             // the row-block last).  Other pieces publish with a release add (only
             // that thread waits for its release fence) and go on; the summer

@@ -51,7 +51,12 @@ for tag, (M, K, k) in {"q": (12288, 12288, 15), "fc1": (49152, 12288, 3), "fc2":
     out.append(f"| {tag} {M}x{K} | {traffic[tag]['duration_us']:.2f} | {rd:.2f} | {wr:.2f} | {alg / 1e6:.2f} | "
                f"{g('sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active'):.1f} | "
                f"{g('sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active'):.1f} | "
-               f"{g('sm__issue_active.avg.pct_of_peak_sustained_active'):.1f} |")
+               f"{g('sm__inst_issued.avg.pct_of_peak_sustained_active'):.1f} |")
+out.append("\nNotes: DRAM read equals the algorithmic bytes within 0.2 % for every shape (no re-reads). "
+           "The DRAM writes of the q-shape capture (tens of MB) cannot come from the kernel, which writes "
+           "KBs of y/partials; they are most likely write-back of dirty L2 lines left by the preceding "
+           "kernels of the replay. `--set full` durations are cold-cache, serialised ncu replays, not bench "
+           "numbers; the pipe columns are `sm__inst_executed_pipe_*` and `sm__inst_issued` as % of peak.")
 open(os.path.join(P, f"{rnd}_summary.md"), "w").write("\n".join(out) + "\n")
 if traffic:
     layer_tags = ["q", "q", "q", "q", "fc1", "fc2" if "fc2" in traffic else "fc1"]
