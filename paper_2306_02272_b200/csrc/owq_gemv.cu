@@ -380,24 +380,31 @@ __device__ __forceinline__ int group_of(const Params& p, int li) { return p.g.gr
 template <int BITS, int NN, int DWG_>
 struct Cfg {
   static constexpr int DWG = DWG_;
+  // MMA issuers per decode warpgroup: with 2, issuer i owns A buffer i (stages
+  // alternate), so consecutive stages' MMAs issue concurrently (own D each).
+  // Implemented, but measured slower at batch 1 (the decode becomes the limit and
+  // the extra MMA concurrency adds TMEM contention): 1 everywhere.
+  static constexpr int ISS = 1;
   // In-kernel digit mode (decode warps turn the stage's raw x into digit tiles,
   // no pre-pass) is implemented but off: measured slower on B200 (12288^2 B=1:
   // 28.2 us vs 24.0 us) because it lengthens the decode warps' stage.
   static constexpr bool kInDig = false;
-  static constexpr int kIPW0 = (512 - 2 * DWG * NN) / (2 * DWG * 16);
+  static constexpr int kIPW0 = (512 - 2 * ISS * DWG * NN) / (2 * DWG * 16);
   static constexpr int kIPW = kIPW0 > 6 ? 6 : kIPW0;
   static constexpr int kMaxB = NN == 8 ? 1 : NN == 16 ? 2 : NN == 32 ? 5 : NN == 64 ? 10 : 16;
   static constexpr int kDecodeWarps = 4 * DWG;            // DWG decode warpgroups
   static constexpr int kEpiWarp0 = kDecodeWarps;          // 4 epilogue warps (warp % 4 = TMEM lane quarter)
-  static constexpr int kMmaWarp0 = kEpiWarp0 + 4;         // one MMA-issuer warp per warpgroup
-  static constexpr int kProdWarp = kMmaWarp0 + DWG;
-  static constexpr int kWarps = kProdWarp + 1;
+  static constexpr int kMmaWarp0 = kEpiWarp0 + 4;         // ISS MMA-issuer warps per warpgroup
+  static constexpr int kProdWarp = kMmaWarp0 + DWG * ISS;
+  // 17 warps would put 5 on one SMSP with the 120 registers __launch_bounds__ allows
+  // -> launch failure; pad that case to 20 (96 registers)
+  static constexpr int kWarps = ISS == 2 ? (kProdWarp + 1 + 3) / 4 * 4 : kProdWarp + 1;
   static constexpr int kThreads = kWarps * 32;
   static constexpr int kTmemCols = 512;
   static constexpr int kACols = kSuperStep / 4;           // 16 TMEM columns (4 code bytes each) per item
   static constexpr int kABuf = kIPW * kACols;            // TMEM columns per A buffer
-  static constexpr int kDCol0 = DWG * 2 * kABuf;          // A: [DWG][2] buffers, then D: [DWG][2] x NN columns
-  static_assert(kDCol0 + DWG * 2 * NN <= kTmemCols, "TMEM budget");
+  static constexpr int kDCol0 = DWG * 2 * kABuf;          // A: [DWG][2] buffers, then D: [DWG*ISS][2] x NN columns
+  static_assert(kDCol0 + DWG * ISS * 2 * NN <= kTmemCols, "TMEM budget");
   static_assert(kMaxB * kDigits <= NN, "digit rows");
   // per stage: decode warps arrive, each MMA warp commits (B is read from the stage)
   static constexpr int kEmptyCount = kDecodeWarps + DWG;
@@ -469,9 +476,10 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
   uint64_t* empty = full + NST;
   uint64_t* afull = empty + NST;       // [DWG][2]  A buffer written (4 warps)
   uint64_t* aempty = afull + DWG * 2;  // [DWG][2]  MMA done reading it
-  uint64_t* dfull = aempty + DWG * 2;  // [DWG][2]  group accumulator complete
-  uint64_t* dempty = dfull + 2 * DWG;  // [DWG][2]  epilogue drained it
-  uint64_t* tready = dempty + 2 * DWG;  // [NST]  digit tiles of the stage landed (TMA tx); only the MMA waits on it
+  constexpr int NDQ = DWG * C::ISS;    // D accumulator owners (warpgroup, issuer)
+  uint64_t* dfull = aempty + DWG * 2;  // [NDQ][2]  group accumulator complete
+  uint64_t* dempty = dfull + 2 * NDQ;  // [NDQ][2]  epilogue drained it
+  uint64_t* tready = dempty + 2 * NDQ;  // [NST]  digit tiles of the stage landed (TMA tx); only the MMA waits on it
   StageDesc* desc = reinterpret_cast<StageDesc*>(tready + NST);       // [NST]
   uint4* mbox = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(desc + NST) + 15) & ~(uintptr_t)15);   // [DWG][2] decode -> MMA notes
   int64_t* span = reinterpret_cast<int64_t*>(mbox + 2 * DWG);         // [2] this CTA's item range
@@ -484,9 +492,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
     span[0] = p.span[cta];
     span[1] = p.span[cta + 1];
     for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); mbar_init(&tready[s], 1); }
-    for (int i = 0; i < 2 * DWG; ++i) {
-      mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4);
-    }
+    for (int i = 0; i < 2 * DWG; ++i) { mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); }
+    for (int i = 0; i < 2 * NDQ; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == C::kProdWarp) {
@@ -607,8 +614,9 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
       if (q == 0) mbar_wait(&full[s], ph);
       named_sync(bar_id, 128);
       const StageDesc d = load_desc(&desc[s]);
-      const bool code = d.n > 0 && d.li < nss;
-      if (code || d.n == 0) {
+      if (d.n == 0) break;   // the MMA warps walk the stage sequence themselves: no terminal note
+      const bool code = d.li < nss;
+      if (code) {
         const uint32_t buf = acnt & 1u;
         if (acnt >= 2) {
           if (q == 0) mbar_wait(&aempty[wg * 2 + buf], ((acnt >> 1) & 1u) ^ 1u);
@@ -694,104 +702,139 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
                                           (uint32_t)d.rb);
         __syncwarp();
         if (lane == 0) mbar_arrive(&afull[wg * 2 + buf]);
-        if (d.n == 0) break;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == NST) { s = 0; ph ^= 1u; }
     }
-  } else if (warp >= C::kMmaWarp0) {
-    // ==================================================================== MMA issue (one warp per warpgroup)
-    // Driven by the decode warpgroup's notes (afull + mailbox).  The whole warp
-    // runs this (warp-uniform control flow); one elected lane issues each
-    // tcgen05.mma / commit.
-    const int wg = warp - C::kMmaWarp0;
-    uint32_t acnt = 0, dcnt = 0;
+  } else if (warp >= C::kMmaWarp0 && warp < C::kProdWarp) {
+    // ==================================================================== MMA issue (ISS warps per warpgroup)
+    // Each issuer walks the CTA's code-stage sequence itself (the producer's
+    // partition).  Stage j goes to A buffer j & 1; issuer ii of warpgroup wg
+    // issues the stages with (j & 1) == ii (every stage when ISS == 1) into its
+    // own D accumulators, and commits its D (dfull) at every end of a scale group
+    // it has open -- also when the group ends in the other issuer's stage.  The
+    // whole warp runs this (warp-uniform); one elected lane issues each mma/commit.
+    constexpr int ISS = C::ISS;
+    const int wq = warp - C::kMmaWarp0, wg = wq / ISS, ii = wq % ISS;
+    const int dq = wg * ISS + ii;                       // D owner index
+    uint32_t dcnt = 0;
     bool open = false;          // D[dcnt & 1] holds a partial group sum
+    int64_t orb = -1;
+    int ogi = -1;               // the open group's row-block and group
+    const int gl = g.group ? p.group_log2 : 30;
     const uint32_t a_wg = tmem + (uint32_t)(wg * 2 * C::kABuf);
     constexpr uint32_t kLbo = (NN / 8) * 128;          // K-adjacent core matrices
     const uint32_t ring0 = smem_addr(ring) + (uint32_t)p.tile_off;
-    int kst = 0;
     long long c_wait = 0, c_issue = 0, c_commit = 0, c_mma = 0, c_tready = 0, c_dempty = 0;   // trace only
-    for (;;) {
-      const uint32_t buf = acnt & 1u;
-      const long long t0 = clock64();
-      mbar_wait(&afull[wg * 2 + buf], (acnt >> 1) & 1u);
-      const long long t1 = clock64();
-      c_wait += t1 - t0;
-      ++acnt;
-      const uint4 note = mbox[wg * 2 + buf];
-      StageDesc d;
-      d.n = (uint8_t)(note.z & 0xFF);
-      if (d.n == 0) break;
-      d.li = (int16_t)note.y;
-      d.flags = (uint8_t)(note.z >> 24);
-      d.rb = (int32_t)note.w;
-      const int s = (int)(note.x & 0x7FFFFFFFu), lo = (int)((note.z >> 8) & 0xFF), hi = (int)((note.z >> 16) & 0xFF);
-      const long long tt0 = clock64();
-      if (!C::kInDig) mbar_wait(&tready[s], note.x >> 31);   // this stage's digit tiles
-      c_tready += clock64() - tt0;
-      if (p.trace && wg == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
-      tc_fence_after();
-      const uint32_t stile = ring0 + (uint32_t)s * (uint32_t)p.stage_bytes;
-      if (!p.g.group && hi - lo == C::kIPW) {
-        // common case: one scale group, full share -> one asm block, one elect
-        const uint32_t dbuf = dcnt & 1u;
-        const long long td0 = clock64();
-        if (!open && dcnt >= 2) mbar_wait(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
-        c_dempty += clock64() - td0;
-        tc_mma_i8_stage<C::kIPW, NN * kSuperStep, kLbo>(
-            tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * NN), a_wg + buf * (uint32_t)C::kABuf,
-            umma_desc(stile + (uint32_t)lo * tile_bytes, kLbo, 128), idesc_i8<NN>(), open ? 1u : 0u);
-        open = true;
-        c_mma += 2 * C::kIPW;
-        if (!(d.flags & kGroupCont)) {
-          tc_commit_elect(&dfull[wg * 2 + dbuf]);
-          ++dcnt;
-          open = false;
-        }
-      } else
-      for (int pa = 0; pa < d.n;) {
-        const Seg sg = segment(p, pa, d);
-        const int a0 = sg.pa > lo ? sg.pa : lo, a1 = sg.pb + 1 < hi ? sg.pb + 1 : hi;
-        for (int pi = a0; pi < a1; ++pi) {
+    auto close_group = [&]() {
+      tc_commit_elect(&dfull[dq * 2 + (dcnt & 1u)]);
+      ++dcnt;
+      open = false;
+    };
+    StageIter it;
+    it.init(g, i0, i1, p.cap);
+    auto next_code = [&](int64_t& rb_, int32_t& li_) {
+      int32_t m;
+      while ((m = it.next(rb_, li_)) > 0 && li_ >= g.nss) {}
+      return m;
+    };
+    int64_t srb, nrb = -1;
+    int32_t sli, nli = 0;
+    int32_t n = next_code(srb, sli);
+    int j = 0, kst = 0;
+    while (n > 0) {
+      const int32_t nn = next_code(nrb, nli);
+      const uint32_t buf = (uint32_t)j & 1u;
+      const int s = j % NST;
+      if (ISS == 1 || (int)buf == ii) {
+        const long long t0 = clock64();
+        mbar_wait(&afull[wg * 2 + buf], ((uint32_t)j >> 1) & 1u);
+        const long long t1 = clock64();
+        c_wait += t1 - t0;
+        int lo, hi;
+        share<DWG>(n, wg, lo, hi);
+        if (!C::kInDig) mbar_wait(&tready[s], (uint32_t)(j / NST) & 1u);   // this stage's digit tiles
+        c_tready += clock64() - t1;
+        if (p.trace && dq == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
+        tc_fence_after();
+        const uint32_t stile = ring0 + (uint32_t)s * (uint32_t)p.stage_bytes;
+        const bool cont = nn > 0 && nrb == srb && ((nli >> gl) == ((sli + n - 1) >> gl));   // last group continues
+        if (!p.g.group && hi - lo == C::kIPW) {
+          // common case: one scale group, full share -> one asm block, one elect
           const uint32_t dbuf = dcnt & 1u;
-          if (!open && dcnt >= 2) mbar_wait(&dempty[wg * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
-          const uint32_t a_t = a_wg + buf * (uint32_t)C::kABuf + (uint32_t)(pi - lo) * C::kACols;
-          const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (wg * 2 + dbuf) * NN);
-          const uint32_t tb = stile + (uint32_t)pi * tile_bytes;
-#pragma unroll
-          for (int j = 0; j < 2; ++j)   // K = 32 columns each: TMEM columns 8j.., core-matrix K-chunks 2j, 2j+1
-            tc_mma_i8_elect(d_t, a_t + 8 * j, umma_desc(tb + j * 2 * kLbo, kLbo, 128), idesc_i8<NN>(),
-                            (open || j > 0) ? 1u : 0u);
+          const long long td0 = clock64();
+          if (!open && dcnt >= 2) mbar_wait(&dempty[dq * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
+          c_dempty += clock64() - td0;
+          tc_mma_i8_stage<C::kIPW, NN * kSuperStep, kLbo>(
+              tmem + (uint32_t)(C::kDCol0 + (dq * 2 + dbuf) * NN), a_wg + buf * (uint32_t)C::kABuf,
+              umma_desc(stile + (uint32_t)lo * tile_bytes, kLbo, 128), idesc_i8<NN>(), open ? 1u : 0u);
           open = true;
-          c_mma += 2;
+          orb = srb;
+          ogi = 0;
+          c_mma += 2 * C::kIPW;
+          if (!cont) close_group();
+        } else {
+          StageDesc d;
+          d.rb = (int32_t)srb; d.li = (int16_t)sli; d.n = (uint8_t)n; d.flags = cont ? kGroupCont : 0;
+          for (int pa = 0; pa < n;) {
+            const Seg sg = segment(p, pa, d);
+            const int a0 = sg.pa > lo ? sg.pa : lo, a1 = sg.pb + 1 < hi ? sg.pb + 1 : hi;
+            if (open && (orb != srb || ogi != sg.gi)) close_group();   // (cannot happen: closed at its end)
+            for (int pi = a0; pi < a1; ++pi) {
+              const uint32_t dbuf = dcnt & 1u;
+              if (!open && dcnt >= 2) mbar_wait(&dempty[dq * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
+              const uint32_t a_t = a_wg + buf * (uint32_t)C::kABuf + (uint32_t)(pi - lo) * C::kACols;
+              const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (dq * 2 + dbuf) * NN);
+              const uint32_t tb = stile + (uint32_t)pi * tile_bytes;
+#pragma unroll
+              for (int jj = 0; jj < 2; ++jj)   // K = 32 columns each: TMEM columns 8jj.., core-matrix K-chunks 2jj, 2jj+1
+                tc_mma_i8_elect(d_t, a_t + 8 * jj, umma_desc(tb + jj * 2 * kLbo, kLbo, 128), idesc_i8<NN>(),
+                                (open || jj > 0) ? 1u : 0u);
+              open = true;
+              orb = srb;
+              ogi = sg.gi;
+              c_mma += 2;
+            }
+            if (sg.ends && open) close_group();
+            pa = sg.pb + 1;
+          }
         }
-        if (sg.ends && open) {
-          tc_commit_elect(&dfull[wg * 2 + (dcnt & 1u)]);
-          ++dcnt;
-          open = false;
+        const long long t2 = clock64();
+        tc_commit_elect(&aempty[wg * 2 + buf]);   // A buffer consumed once these MMAs complete
+        tc_commit_elect(&empty[s]);                // ... and the stage's digit tiles
+        const long long t3 = clock64();
+        c_issue += t2 - t1;
+        c_commit += t3 - t2;
+        if (p.trace && dq == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
+        ++kst;
+      } else if (open) {
+        // the other issuer's stage: does my open group end inside it?
+        bool ends;
+        if (orb != srb || (sli >> gl) != ogi) {
+          ends = true;   // (defensive: the group ended before this stage)
+        } else {
+          const bool later = ((sli + n - 1) >> gl) != ogi;   // the stage reaches a later group
+          const bool cont = nn > 0 && nrb == srb && (nli >> gl) == ogi;
+          ends = later || !cont;
         }
-        pa = sg.pb + 1;
+        if (ends) close_group();
       }
-      const long long t2 = clock64();
-      tc_commit_elect(&aempty[wg * 2 + buf]);   // A buffer consumed once these MMAs complete
-      tc_commit_elect(&empty[s]);                // ... and the stage's digit tiles
-      const long long t3 = clock64();
-      c_issue += t2 - t1;
-      c_commit += t3 - t2;
-      if (p.trace && wg == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
-      ++kst;
+      ++j;
+      srb = nrb;
+      sli = nli;
+      n = nn;
     }
+    if (open) close_group();
     if (p.trace && lane == 0) {
-      p.trace[cta * 256 + 1 + wg] = (unsigned long long)c_wait;
-      p.trace[cta * 256 + 5 + wg] = (unsigned long long)c_issue;
-      p.trace[cta * 256 + 9 + wg * 0] = (unsigned long long)c_commit;
+      p.trace[cta * 256 + 1 + dq] = (unsigned long long)c_wait;
+      p.trace[cta * 256 + 5 + dq] = (unsigned long long)c_issue;
+      p.trace[cta * 256 + 9 + dq * 0] = (unsigned long long)c_commit;
       p.trace[cta * 256 + 52] = (unsigned long long)c_mma;
-      p.trace[cta * 256 + 42 + wg] = (unsigned long long)c_tready;
-      p.trace[cta * 256 + 46 + wg] = (unsigned long long)c_dempty;
+      p.trace[cta * 256 + 42 + dq] = (unsigned long long)c_tready;
+      p.trace[cta * 256 + 46 + dq] = (unsigned long long)c_dempty;
     }
-  } else {
+  } else if (warp >= C::kEpiWarp0 && warp < C::kMmaWarp0) {
     // ==================================================================== epilogue
     // Independent of the shared-memory ring: walks this CTA's item sequence
     // itself (the producer's stage partition, without waiting on stages),
@@ -816,10 +859,12 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
     long long sacc[MAXB];                                // this thread's share of the open group's digit sums
 #pragma unroll
     for (int b = 0; b < MAXB; ++b) { tot[b] = 0.f; sacc[b] = 0; }
-    uint32_t dcnt[DWG];
+    constexpr int ISS = C::ISS;
+    uint32_t dcnt[NDQ];
 #pragma unroll
-    for (int w = 0; w < DWG; ++w) dcnt[w] = 0;
-    uint32_t part = 0;                                   // warpgroups with items in the open group
+    for (int w = 0; w < NDQ; ++w) dcnt[w] = 0;
+    uint32_t part = 0;                                   // D owners (warpgroup, issuer) with items in the open group
+    int jc = 0;                                          // code-stage index (stage j -> issuer j & 1 when ISS == 2)
     bool gopen = false;
     uint32_t szw = 0;                                    // the open group's (s, z) for this row
     uint4 wpre[2];                                       // this row's first two weak chunks of the row-block (prefetch)
@@ -881,14 +926,18 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
               for (int b = 0; b < MAXB; ++b)
                 if (b < p.B) sacc[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
           }
-          if (cn == p.cap && !g.group) {
-            part = (1u << DWG) - 1u;   // full stage, one segment: every warpgroup has items
-          } else {
+          {
+            const int iss = ISS == 1 ? 0 : (jc & 1);
+            if (cn == p.cap && !g.group) {   // full stage, one segment: every warpgroup has items
 #pragma unroll
-            for (int w = 0; w < DWG; ++w) {
-              int lo, hi;
-              share<DWG>(cn, w, lo, hi);
-              if (lo <= pb && hi > pa) part |= 1u << w;
+              for (int w = 0; w < DWG; ++w) part |= 1u << (w * ISS + iss);
+            } else {
+#pragma unroll
+              for (int w = 0; w < DWG; ++w) {
+                int lo, hi;
+                share<DWG>(cn, w, lo, hi);
+                if (lo <= pb && hi > pa) part |= 1u << (w * ISS + iss);
+              }
             }
           }
           if (ends) {
@@ -943,8 +992,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
 #pragma unroll
             for (int b = 0; b < MAXB; ++b) dacc[b] = 0.0;
 #pragma unroll
-            for (int w = 0; w < DWG; ++w) {
-              if (part & (1u << w)) {   // fixed order over warpgroups: deterministic
+            for (int w = 0; w < NDQ; ++w) {
+              if (part & (1u << w)) {   // fixed order over D owners: deterministic
                 const uint32_t dbuf = dcnt[w] & 1u;
                 // one warp waits (suspending), the others block on the named barrier
                 if (q == 0) mbar_wait(&dfull[w * 2 + dbuf], (dcnt[w] >> 1) & 1u);
@@ -978,6 +1027,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
           }
           pa = pb + 1;
         }
+        ++jc;
       } else {
         // weak chunks (straight from the blob, not through the ring): fp16 weak
         // columns x gathered activations, fp32 (unscaled)
@@ -1276,8 +1326,8 @@ static owq_status launch_n(const Params& p, int64_t grid, cudaStream_t cs) {
       if (dwg == 3) return launch<BITS, 8, 3>(p, grid, cs);
       if (dwg == 4) return launch<BITS, 8, 4>(p, grid, cs);
       return launch<BITS, 8, 2>(p, grid, cs);
-    case 16: return launch<BITS, 16, 4>(p, grid, cs);
-    case 32: return launch<BITS, 32, 4>(p, grid, cs);
+    case 16: return launch<BITS, 16, 3>(p, grid, cs);
+    case 32: return launch<BITS, 32, 3>(p, grid, cs);
     case 64: return launch<BITS, 64, 2>(p, grid, cs);
     default: return launch<BITS, 96, 2>(p, grid, cs);
   }
