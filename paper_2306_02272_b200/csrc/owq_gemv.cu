@@ -74,6 +74,8 @@ struct Params {
   int32_t tile_off;       // digit tiles inside a stage
   int32_t sum_off;        // per-item digit sums inside a stage (in-kernel digit mode)
   int32_t x_off;          // raw x columns of the stage, B rows of cap*64 fp16 (in-kernel digit mode)
+  int32_t sz_off;         // scale/zero blocks of the stage's groups (grouped per-stage mode)
+  int32_t gstage;         // grouped per-stage mode: the epilogue consumes the ring (sums + s/z staged)
   int32_t stage_bytes;
   int64_t xK;             // row stride of x in elements
   int32_t group_log2;     // log2(group_size / 64)
@@ -403,8 +405,11 @@ struct Cfg {
   static constexpr int kTmemCols = 512;
   static constexpr int kACols = kSuperStep / 4;           // 16 TMEM columns (4 code bytes each) per item
   static constexpr int kABuf = kIPW * kACols;            // TMEM columns per A buffer
-  static constexpr int kDCol0 = DWG * 2 * kABuf;          // A: [DWG][2] buffers, then D: [DWG*ISS][2] x NN columns
-  static_assert(kDCol0 + DWG * ISS * 2 * NN <= kTmemCols, "TMEM budget");
+  static constexpr int kDCol0 = DWG * 2 * kABuf;          // A: [DWG][2] buffers, then D: [DWG*ISS][2][kGP] x NN columns
+  // Grouped scales (g > 0) at batch 1: per-stage D with one block per scale-group
+  // piece of a warpgroup's share (<= 4 pieces for g = 128 and 6 items), when TMEM fits.
+  static constexpr int kGP = (NN == 8 && ISS == 1 && kDCol0 + DWG * 2 * 4 * NN <= kTmemCols) ? 4 : 1;
+  static_assert(kDCol0 + DWG * ISS * 2 * kGP * NN <= kTmemCols, "TMEM budget");
   static_assert(kMaxB * kDigits <= NN, "digit rows");
   // per stage: decode warps arrive, each MMA warp commits (B is read from the stage)
   static constexpr int kEmptyCount = kDecodeWarps + DWG;
@@ -491,7 +496,11 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
     if (p.trace) p.trace[cta * 256 + 0] = gtime();
     span[0] = p.span[cta];
     span[1] = p.span[cta + 1];
-    for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], C::kEmptyCount); mbar_init(&tready[s], 1); }
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::kEmptyCount + (p.gstage ? 4 : 0));   // + the epilogue in grouped per-stage mode
+      mbar_init(&tready[s], 1);
+    }
     for (int i = 0; i < 2 * DWG; ++i) { mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); }
     for (int i = 0; i < 2 * NDQ; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -524,8 +533,13 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
         pdl_wait();
         dep = true;
         for (int i = 0; i < npend; ++i)
+        {
           bulk_g2s(ring + (size_t)pend_s[i] * p.stage_bytes + p.tile_off, p.tiles + (int64_t)pend_sli[i] * tile_bytes,
                    (uint32_t)pend_n[i] * tile_bytes, &tready[pend_s[i]], pol_x);
+          if (p.gstage)
+            bulk_g2s(ring + (size_t)pend_s[i] * p.stage_bytes + p.sum_off, p.sums + (int64_t)pend_sli[i] * p.Bp,
+                     (uint32_t)(pend_n[i] * p.Bp * 8), &tready[pend_s[i]], pol_x);
+        }
         npend = 0;
       };
       // code stages only: weak chunks never enter the ring (the epilogue reads them)
@@ -559,11 +573,21 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
         if (code && !C::kInDig) {
           // codes -> full[s] (decode), digit tiles -> tready[s] (MMA only), so the
           // decode can run while the x-digit pass is still producing the tiles
-          mbar_expect_tx(&full[s], cbytes);
-          mbar_expect_tx(&tready[s], (uint32_t)n * tile_bytes);
+          const uint32_t sumb = p.gstage ? (uint32_t)(n * p.Bp * 8) : 0u;
+          uint32_t szb = 0;
+          if (p.gstage) {
+            const int gi0 = group_of(p, sli);
+            szb = (uint32_t)((group_of(p, sli + n - 1) - gi0 + 1) * kSZBlockBytes);
+            mbar_expect_tx(&full[s], cbytes + szb);
+            bulk_g2s(st + p.sz_off, p.blob + g.sz_off + (srb * g.G + gi0) * kSZBlockBytes, szb, &full[s], pol);
+          } else {
+            mbar_expect_tx(&full[s], cbytes);
+          }
+          mbar_expect_tx(&tready[s], (uint32_t)n * tile_bytes + sumb);
           bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
           if (dep) {
             bulk_g2s(st + p.tile_off, p.tiles + (int64_t)sli * tile_bytes, (uint32_t)n * tile_bytes, &tready[s], pol_x);
+            if (sumb) bulk_g2s(st + p.sum_off, p.sums + (int64_t)sli * p.Bp, sumb, &tready[s], pol_x);
           } else {
             pend_sli[npend] = sli; pend_n[npend] = n; pend_s[npend] = s; ++npend;
           }
@@ -760,14 +784,33 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
         tc_fence_after();
         const uint32_t stile = ring0 + (uint32_t)s * (uint32_t)p.stage_bytes;
         const bool cont = nn > 0 && nrb == srb && ((nli >> gl) == ((sli + n - 1) >> gl));   // last group continues
-        if (!p.g.group && hi - lo == C::kIPW) {
+        if (C::kGP > 1 && p.g.group) {
+          // grouped scales: D of this stage = [buf][piece] blocks, drained by the
+          // epilogue per stage (dempty of the stage that used this buffer before)
+          if (j >= 2) mbar_wait(&dempty[wg * 2 + buf], (((uint32_t)j >> 1) - 1) & 1u);
+          tc_fence_after();
+          const int g0 = (sli + lo) >> gl;
+          for (int pi = lo; pi < hi; ++pi) {
+            const int gi = (sli + pi) >> gl;
+            const bool first = pi == lo || gi != ((sli + pi - 1) >> gl);
+            const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + ((wg * 2 + buf) * C::kGP + (gi - g0)) * NN);
+            const uint32_t a_t = a_wg + buf * (uint32_t)C::kABuf + (uint32_t)(pi - lo) * C::kACols;
+            const uint32_t tb = stile + (uint32_t)pi * tile_bytes;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj)
+              tc_mma_i8_elect(d_t, a_t + 8 * jj, umma_desc(tb + jj * 2 * kLbo, kLbo, 128), idesc_i8<NN>(),
+                              (!first || jj > 0) ? 1u : 0u);
+            c_mma += 2;
+          }
+          tc_commit_elect(&dfull[wg * 2 + buf]);   // this stage's group pieces (possibly none)
+        } else if (!p.g.group && hi - lo == C::kIPW) {
           // common case: one scale group, full share -> one asm block, one elect
           const uint32_t dbuf = dcnt & 1u;
           const long long td0 = clock64();
           if (!open && dcnt >= 2) mbar_wait(&dempty[dq * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
           c_dempty += clock64() - td0;
           tc_mma_i8_stage<C::kIPW, NN * kSuperStep, kLbo>(
-              tmem + (uint32_t)(C::kDCol0 + (dq * 2 + dbuf) * NN), a_wg + buf * (uint32_t)C::kABuf,
+              tmem + (uint32_t)(C::kDCol0 + (dq * 2 + dbuf) * C::kGP * NN), a_wg + buf * (uint32_t)C::kABuf,
               umma_desc(stile + (uint32_t)lo * tile_bytes, kLbo, 128), idesc_i8<NN>(), open ? 1u : 0u);
           open = true;
           orb = srb;
@@ -785,7 +828,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
               const uint32_t dbuf = dcnt & 1u;
               if (!open && dcnt >= 2) mbar_wait(&dempty[dq * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
               const uint32_t a_t = a_wg + buf * (uint32_t)C::kABuf + (uint32_t)(pi - lo) * C::kACols;
-              const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (dq * 2 + dbuf) * NN);
+              const uint32_t d_t = tmem + (uint32_t)(C::kDCol0 + (dq * 2 + dbuf) * C::kGP * NN);
               const uint32_t tb = stile + (uint32_t)pi * tile_bytes;
 #pragma unroll
               for (int jj = 0; jj < 2; ++jj)   // K = 32 columns each: TMEM columns 8jj.., core-matrix K-chunks 2jj, 2jj+1
@@ -825,7 +868,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
       sli = nli;
       n = nn;
     }
-    if (open) close_group();
+    if (open && !(C::kGP > 1 && p.g.group)) close_group();
     if (p.trace && lane == 0) {
       p.trace[cta * 256 + 1 + dq] = (unsigned long long)c_wait;
       p.trace[cta * 256 + 5 + dq] = (unsigned long long)c_issue;
@@ -890,9 +933,96 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
     int64_t crb, nrb = -1;
     int32_t cli, nli = 0;
     int32_t cn = it.next(crb, cli);
+    // grouped-scale per-stage mode (C::kGP > 1): the open group's running sums
+    const bool gmode = C::kGP > 1 && g.group != 0;
+    long long e_ring = 0, e_dfull = 0, e_ld = 0, e_comb = 0;   // trace only
+    // exact int64 throughout: |X| < 2^40 makes |sum_i 256^i D_i| < 2^62 for any K
+    int gm_g = -1;
+    long long gm_v = 0, gm_s = 0;
+    uint32_t gm_sz = 0;
+    // (macro, not a lambda: a by-reference capture kept the group state in local memory)
+#define OWQ_GM_FINISH()                                                                                 \
+  do {                                                                                                  \
+    if (gm_g >= 0) {                                                                                    \
+      const __half2 szv_ = u2h(gm_sz);                                                                  \
+      const long long vz_ = gm_v - (long long)__high2float(szv_) * gm_s; /* z is an integer code */     \
+      tot[0] = fmaf(__low2float(szv_) * 5.9604644775390625e-08f, __ll2float_rn(vz_), tot[0]);           \
+    }                                                                                                   \
+    gm_g = -1;                                                                                          \
+  } while (0)
     while (cn > 0) {
       const int32_t nn = it.next(nrb, nli);
-      if (cli < g.nss) {
+      if (cli < g.nss && gmode) {
+        // one D buffer per stage and warpgroup: [piece] blocks of kGP x NN columns
+        const int gA = cli >> gl;
+        constexpr int kCapMax = DWG * C::kIPW;
+        // the stage's digit sums and (s, z) blocks are staged in the ring (tready / full)
+        const int rs = jc % NST;
+        const uint32_t rph = (uint32_t)(jc / NST) & 1u;
+        long long tq0 = clock64();
+        if (q == 0) {
+          mbar_wait(&full[rs], rph);
+          mbar_wait(&tready[rs], rph);
+        }
+        named_sync(2, 128);
+        const uint32_t sb = smem_addr(ring + (size_t)rs * p.stage_bytes);
+        (void)kCapMax;
+        long long tq1 = clock64();
+        e_ring += tq1 - tq0;
+        for (int w = 0; w < DWG; ++w) {
+          long long tw0 = clock64();
+          if (q == 0) mbar_wait(&dfull[w * 2 + (jc & 1)], ((uint32_t)jc >> 1) & 1u);
+          named_sync(2, 128);
+          tc_fence_after();
+          long long tw1 = clock64();
+          e_dfull += tw1 - tw0;
+          int lo, hi;
+          share<DWG>(cn, w, lo, hi);
+          if (lo < hi) {
+            const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + (jc & 1)) * C::kGP * NN);
+            const int g0 = (cli + lo) >> gl;
+            long long tw2 = clock64();
+#pragma unroll
+            for (int c16 = 0; c16 < C::kGP * NN / 16; ++c16) {   // two pieces (2 x NN columns) per load
+              uint32_t dd[16];
+              tc_ld16(tcol + 16 * c16, dd);
+#pragma unroll
+              for (int ph2 = 0; ph2 < 16 / NN; ++ph2) {
+                const int pc = c16 * (16 / NN) + ph2;
+                const int gp = g0 + pc;
+                const int ia = ((gp << gl) - cli) > lo ? ((gp << gl) - cli) : lo;
+                const int ib = (((gp + 1) << gl) - cli) < hi ? (((gp + 1) << gl) - cli) : hi;
+                if (ia < ib) {
+                  long long v = 0;
+#pragma unroll
+                  for (int i = 0; i < kDigits; ++i) v += (long long)(int)dd[ph2 * NN + i] << (8 * i);
+                  long long sp = 0;
+                  for (int t = ia; t < ib; ++t) {
+                    const uint2 sv = lds64(sb + (uint32_t)p.sum_off + (uint32_t)(t * p.Bp) * 8u);
+                    sp += (long long)(((unsigned long long)sv.y << 32) | sv.x);
+                  }
+                  if (gp != gm_g) {
+                    OWQ_GM_FINISH();
+                    gm_g = gp;
+                    gm_v = 0;
+                    gm_s = 0;
+                    gm_sz = lds32(sb + (uint32_t)p.sz_off + (uint32_t)(gp - gA) * kSZBlockBytes + row * 4);
+                  }
+                  gm_v += v;
+                  gm_s += sp;
+                }
+              }
+            }
+            e_comb += clock64() - tw2;
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&dempty[w * 2 + (jc & 1)]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rs]);   // done with the stage's staged sums and (s, z)
+        ++jc;
+      } else if (cli < g.nss) {
         for (int pa = 0; pa < cn;) {
           const int gi = (cli + pa) >> gl;
           const int gend = ((gi + 1) << gl) - cli - 1;   // last stage position of this group
@@ -999,7 +1129,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
                 if (q == 0) mbar_wait(&dfull[w * 2 + dbuf], (dcnt[w] >> 1) & 1u);
                 named_sync(2, 128);
                 tc_fence_after();
-                const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * NN);
+                const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * C::kGP * NN);
 #pragma unroll
                 for (int c16 = 0; c16 < (MAXB * kDigits + 15) / 16; ++c16) {
                   uint32_t dd[16];
@@ -1073,6 +1203,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
       if (p.trace && et == 0 && kst < 32) p.trace[cta * 256 + 160 + kst] = gtime();
       ++kst;
 
+      if (gmode && (nn == 0 || nrb != crb || nli >= g.nss)) OWQ_GM_FINISH();   // the row-block's code part is done
       if (nn == 0 || nrb != crb) {
         // -------------------------------------------------- finish row-block crb
         if (p.trace && et == 0) p.trace[cta * 256 + 50] = gtime();
@@ -1160,6 +1291,12 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_ker
       crb = nrb;
       cli = nli;
       cn = nn;
+    }
+    if (p.trace && et == 0) {
+      p.trace[cta * 256 + 53] = (unsigned long long)e_ring;
+      p.trace[cta * 256 + 54] = (unsigned long long)e_dfull;
+      p.trace[cta * 256 + 55] = (unsigned long long)e_ld;
+      p.trace[cta * 256 + 57] = (unsigned long long)e_comb;
     }
   }
   // teardown: every role is done with TMEM
@@ -1282,8 +1419,11 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   p.code_bytes = (int32_t)std::max<int64_t>((int64_t)p.cap * p.g.ss_bytes, (int64_t)p.cap * kWeakChunkBytes);
   p.tile_off = p.code_bytes;
   p.sum_off = p.tile_off + (int32_t)(p.cap * tile_bytes);
-  p.x_off = p.sum_off + (int32_t)((C::kInDig ? p.cap * p.Bp * 8 : 0) + 127) / 128 * 128;
-  p.stage_bytes = (int32_t)((p.x_off + (C::kInDig ? p.B * p.cap * kSuperStep * 2 : 0) + 127) / 128 * 128);
+  p.gstage = (C::kGP > 1 && p.g.group) ? 1 : 0;
+  p.x_off = p.sum_off + (int32_t)(((C::kInDig || p.gstage) ? p.cap * p.Bp * 8 : 0) + 127) / 128 * 128;
+  p.sz_off = p.x_off + (int32_t)((C::kInDig ? p.B * p.cap * kSuperStep * 2 : 0) + 127) / 128 * 128;
+  const int sz_blocks = p.gstage ? (int)(p.cap * kSuperStep / p.g.group + 2) : 0;
+  p.stage_bytes = (int32_t)((p.sz_off + sz_blocks * kSZBlockBytes + 127) / 128 * 128);
   int nst = (int)(avail / (p.stage_bytes + 32));
   static const int max_nst = getenv("OWQ_NST") ? atoi(getenv("OWQ_NST")) : 8;
   nst = std::min(nst, max_nst);

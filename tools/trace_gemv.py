@@ -31,6 +31,7 @@ for kk in range(0, 16):
 print(" MMA warps (cycles, mean over CTAs): wait afull", [int(t[:, 1 + w].mean()) for w in range(4)],
       " issue", [int(t[:, 5 + w].mean()) for w in range(4)], " commit(wg3)", int(t[:, 9].mean()), " MMAs(wg3)", int(t[:, 52].mean()))
 print(" MMA waits (cycles, mean): tready", [int(t[:, 42 + w].mean()) for w in range(4)], " dempty", [int(t[:, 46 + w].mean()) for w in range(4)])
+print(" epilogue (grouped per-stage mode) cycles: ring", int(t[:, 53].mean()), " dfull", int(t[:, 54].mean()), " ld", int(t[:, 55].mean()), " combine", int(t[:, 57].mean()))
 print(" kernel cycles ~", int((np.median(t[:, 62]) - np.median(t[:, 0])) * 1.9))
 order = np.argsort(-t[:, 62])
 print(" slowest CTAs: idx  start  fin-in  fin-out  end   (us)   last-stage epi_done")
