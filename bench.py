@@ -250,9 +250,11 @@ def graph_upload(g, stream) -> bool:
         return False
 
 
-def launch(L, tp=None):
+def launch(L, tp=None, stream=None):
     import paper_2306_02272_b200 as owq
-    if tp is None or L.get("mode", 0) == 0:
+    if L.get("grid"):
+        owq.owq_gemm_small_batch_grid(L["shape"], L["packed"], L["x"], L["grid"], y=L["y"], ws=L["ws"], stream=stream)
+    elif tp is None or L.get("mode", 0) == 0:
         owq.owq_gemm_small_batch(L["shape"], L["packed"], L["x"], y=L["y"], ws=L["ws"])
     else:
         owq.owq_tp_gemv(tp, L["mode"], L["full"], L["shape"], L["packed"], L["x"], L["y"], ws=L["ws"])
@@ -287,11 +289,40 @@ def run_gpu(args):
         tp = owq.owq_tp_init(obj[0], world, rank)
     step_bytes = sum(L["bytes"] for L in layers)
     stream = torch.cuda.Stream(device=dev)
+    # q, k, v are independent (one input, three weights): on one GPU they run
+    # concurrently on three streams with a third of the SMs each, so their fixed
+    # per-call costs (prologue, pipeline fill/drain, digit pass) overlap; out,
+    # fc1, fc2 depend on their predecessors and run in order on all SMs.
+    concurrent = world == 1 and not args.sequential
+    side = [torch.cuda.Stream(device=dev) for _ in range(3)] if concurrent else []
+    if concurrent:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        qkv = [L for L in layers if L["name"] in ("q", "k", "v")]
+        for j, L in enumerate(qkv):
+            L["grid"] = sms // 3 + (1 if j < sms % 3 else 0)
+            L["ws_seq"] = L["ws"]
+            L["ws"] = owq.workspace(L["shape"], args.batch, dev, grid=L["grid"])
+
+    def step():
+        if not concurrent:
+            for L in layers:
+                launch(L, tp)
+            return
+        cur = torch.cuda.current_stream()
+        for sd in side:
+            sd.wait_stream(cur)
+        for sd, L in zip(side, [L for L in layers if L.get("grid")]):
+            with torch.cuda.stream(sd):
+                launch(L, tp, stream=sd)
+        for sd in side:
+            cur.wait_stream(sd)
+        for L in layers:
+            if not L.get("grid"):
+                launch(L, tp)
     # eager warm-up (verifies blobs, sets kernel attributes) before capture
     with torch.cuda.stream(stream):
         for _ in range(2):
-            for L in layers:
-                launch(L, tp)
+            step()
     torch.cuda.synchronize()
 
     K, W = args.steps, args.warmup
@@ -305,13 +336,11 @@ def run_gpu(args):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
                 for s in range(K):
-                    for L in layers:
-                        launch(L, tp)
+                    step()
             wg = torch.cuda.CUDAGraph()
             with torch.cuda.graph(wg, stream=stream):
                 for _ in range(max(W, 3)):
-                    for L in layers:
-                        launch(L, tp)
+                    step()
         except Exception as e:  # pragma: no cover - fall back to eager timing
             print(f"[bench] graph capture failed ({e}); timing eager launches", file=sys.stderr)
             g = None
@@ -325,8 +354,7 @@ def run_gpu(args):
                 wg.replay()
             else:
                 for _ in range(W):
-                    for L in layers:
-                        launch(L, tp)
+                    step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -338,8 +366,7 @@ def run_gpu(args):
                 g.replay()
             else:
                 for s in range(K):
-                    for L in layers:
-                        launch(L, tp)
+                    step()
             ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -358,8 +385,15 @@ def run_gpu(args):
     for i, L in enumerate(layers):
         shapes.setdefault((L["M"], L["K"]), []).append(i)
     R = max(8, min(2 * K, 60))
+    seq_view = []
+    for L in layers:   # per-launch (roofline) timing: every layer on all SMs
+        Lv = dict(L)
+        Lv.pop("grid", None)
+        if "ws_seq" in L:
+            Lv["ws"] = L["ws_seq"]
+        seq_view.append(Lv)
     for idx in shapes.values():
-        pool = [layers[i] for i in idx]
+        pool = [seq_view[i] for i in idx]
         nbytes = sum(L["bytes"] for L in pool)
         # rotate over >= 3x L2 of distinct weights so every call streams from HBM:
         # extra packed copies for shapes that occur once per step (fc1, fc2)
@@ -401,9 +435,10 @@ def run_gpu(args):
         h2d = sum(h.numel() * 2 for h in xh)
         d2h = sum(h.numel() * 2 for h in yh)
         E = max(3, min(K, 50))
+        eager = seq_view if world == 1 else layers   # one call after another, all SMs
         with torch.cuda.stream(stream):
             for _ in range(3):
-                for h, y_, L in zip(xh, yh, layers):
+                for h, y_, L in zip(xh, yh, eager):
                     L["x"].copy_(h, non_blocking=True)
                     launch(L, tp)
                     y_.copy_(L["y"], non_blocking=True)
@@ -412,7 +447,7 @@ def run_gpu(args):
                 dist.barrier()
             t0 = time.perf_counter()
             for _ in range(E):
-                for h, y_, L in zip(xh, yh, layers):
+                for h, y_, L in zip(xh, yh, eager):
                     L["x"].copy_(h, non_blocking=True)
                     launch(L, tp)
                     y_.copy_(L["y"], non_blocking=True)
@@ -473,6 +508,8 @@ def run_gpu(args):
                    "parallelism": f"tp{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (682 MB of packed weights per step vs 126 MB L2); no flush",
                    "graph": g is not None, "graph_uploaded_before_timing": bool(uploaded) if g is not None else None,
+                   "schedule": ("q, k, v concurrently on 3 streams (a third of the SMs each); out, fc1, fc2 in order"
+                                if concurrent else "all six layers in order on all SMs"),
                    "arith": "codes (u8) x exact int8 digits of x*2^24 on tcgen05.mma kind::i8, s32 accumulate; "
                             "zero point and digits combined exactly (fp64), fp32 scale; weak columns fp16 x fp16, fp32"},
         "us_per_layer": per_layer,
@@ -504,6 +541,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--sequential", action="store_true", help="q, k, v one after another on all SMs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -236,3 +236,47 @@ def test_back_to_back_graph_shared_workspace(dev):
         assert e <= TOL
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
+
+
+def test_concurrent_streams_partial_grids(dev):
+    """The bench's q/k/v schedule: three independent layers on three streams, each
+    on a third of the SMs (explicit grid, own workspace), captured in one graph."""
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    cases = [(2048, 3072, 3, 0, 9), (2048, 3072, 3, 0, 11), (1536, 3072, 4, 0, 5)]
+    main = torch.cuda.Stream()
+    side = [torch.cuda.Stream() for _ in cases]
+    runs = []
+    for i, (M, K, bits, g, k) in enumerate(cases):
+        d = synth.representation(M, K, bits, g, k, seed=300 + i)
+        x = synth.activations(1, K, seed=400 + i, outliers=d["weak_idx"][:4])
+        L = owq.OwqLinear(d, device=dev)
+        grid = sms // 3
+        runs.append(dict(L=L, grid=grid, x=torch.from_numpy(x).to(dev),
+                         y=torch.empty((1, M), dtype=torch.float32, device=dev),
+                         ws=owq.workspace(L.shape, 1, dev, grid=grid),
+                         ref=O.matvec(rep_from_synth(d), x.astype(np.float64))))
+
+    def step():
+        cur = torch.cuda.current_stream()
+        for sd, r in zip(side, runs):
+            sd.wait_stream(cur)
+            with torch.cuda.stream(sd):
+                owq.owq_gemm_small_batch_grid(r["L"].shape, r["L"].packed, r["x"], r["grid"], y=r["y"], y_f32=True,
+                                              ws=r["ws"], stream=sd)
+        for sd in side:
+            cur.wait_stream(sd)
+
+    with torch.cuda.stream(main):
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=main):
+        for _ in range(3):
+            step()
+    for r in runs:
+        r["y"].zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    for r in runs:
+        e, _ = rel_err(r["y"].cpu().numpy().astype(np.float64), r["ref"])
+        assert e <= TOL
