@@ -201,7 +201,7 @@ __device__ __forceinline__ void tc_mma_i8_stage(uint32_t d_t, uint32_t a0, uint6
   "add.u32 a, a, 8;\n\t"                                                                           \
   "add.u64 b, b, %6/16;\n\t"                                                                       \
   "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a], b, %3, p;\n\t"
-  static_assert(IPW >= 1 && IPW <= 6, "IPW");
+  static_assert(IPW >= 1 && IPW <= 7, "IPW");
   if (IPW == 1)
     asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
                  "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) "}" ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc), "r"(acc),
@@ -222,10 +222,14 @@ __device__ __forceinline__ void tc_mma_i8_stage(uint32_t d_t, uint32_t a0, uint6
     asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
                  "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) OWQ_MMA_T(3) OWQ_MMA_T(4) "}"
                  ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
-  else
+  else if (IPW == 6)
     asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
                  "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) OWQ_MMA_T(3) OWQ_MMA_T(4)
                  OWQ_MMA_T(5) "}" ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
+  else
+    asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\telect.sync _|e, 0xffffffff;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t" OWQ_MMA_T(0) OWQ_MMA_T(1) OWQ_MMA_T(2) OWQ_MMA_T(3) OWQ_MMA_T(4)
+                 OWQ_MMA_T(5) OWQ_MMA_T(6) "}" ::"r"(d_t), "r"(a0), "l"(b0), "r"(idesc), "r"(acc), "n"(TILE), "n"(2 * LBO));
 #undef OWQ_MMA_T
 }
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_t, uint32_t a_t, uint64_t b_desc, uint32_t idesc, uint32_t acc) {
@@ -379,7 +383,7 @@ __device__ __forceinline__ int group_of(const Params& p, int li) { return p.g.gr
 // Per (MMA-N class, decode warpgroups): items per warpgroup per stage, largest
 // batch.  Each warpgroup owns two TMEM A buffers (ping-pong) of kIPW items and
 // two D accumulators of NN columns; kIPW is what fits in the 512 TMEM columns.
-template <int BITS, int NN, int DWG_>
+template <int BITS, int NN, int DWG_, bool GRP = false>
 struct Cfg {
   static constexpr int DWG = DWG_;
   // MMA issuers per decode warpgroup: with 2, issuer i owns A buffer i (stages
@@ -392,7 +396,10 @@ struct Cfg {
   // 28.2 us vs 24.0 us) because it lengthens the decode warps' stage.
   static constexpr bool kInDig = false;
   static constexpr int kIPW0 = (512 - 2 * ISS * DWG * NN) / (2 * DWG * 16);
-  static constexpr int kIPW = kIPW0 > 6 ? 6 : kIPW0;
+  // 7 items per warpgroup at batch 1 (measured -8 % vs 6); grouped-scale kernels
+  // keep 6 so the per-stage D blocks (kGP) fit next to the A buffers
+  static constexpr int kIPWMax = GRP ? 6 : 7;
+  static constexpr int kIPW = kIPW0 > kIPWMax ? kIPWMax : kIPW0;
   static constexpr int kMaxB = NN == 8 ? 1 : NN == 16 ? 2 : NN == 32 ? 5 : NN == 64 ? 10 : 16;
   static constexpr int kDecodeWarps = 4 * DWG;            // DWG decode warpgroups
   static constexpr int kEpiWarp0 = kDecodeWarps;          // 4 epilogue warps (warp % 4 = TMEM lane quarter)
@@ -408,7 +415,7 @@ struct Cfg {
   static constexpr int kDCol0 = DWG * 2 * kABuf;          // A: [DWG][2] buffers, then D: [DWG*ISS][2][kGP] x NN columns
   // Grouped scales (g > 0) at batch 1: per-stage D with one block per scale-group
   // piece of a warpgroup's share (<= 4 pieces for g = 128 and 6 items), when TMEM fits.
-  static constexpr int kGP = (NN == 8 && ISS == 1 && kDCol0 + DWG * 2 * 4 * NN <= kTmemCols) ? 4 : 1;
+  static constexpr int kGP = (GRP && NN == 8 && ISS == 1 && kDCol0 + DWG * 2 * 4 * NN <= kTmemCols) ? 4 : 1;
   static_assert(kDCol0 + DWG * ISS * 2 * kGP * NN <= kTmemCols, "TMEM budget");
   static_assert(kMaxB * kDigits <= NN, "digit rows");
   // per stage: decode warps arrive, each MMA warp commits (B is read from the stage)
@@ -465,9 +472,9 @@ __device__ __forceinline__ StageDesc load_desc(const StageDesc* d) {
   return r;
 }
 
-template <int BITS, int NN, int DWG_>
-__global__ void __launch_bounds__(Cfg<BITS, NN, DWG_>::kThreads, 1) owq_gemv_kernel(const Params p) {
-  using C = Cfg<BITS, NN, DWG_>;
+template <int BITS, int NN, int DWG_, bool GRP>
+__global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gemv_kernel(const Params p) {
+  using C = Cfg<BITS, NN, DWG_, GRP>;
   constexpr int DWG = C::DWG, MAXB = C::kMaxB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geo& g = p.g;
@@ -1398,9 +1405,9 @@ static size_t ws_bytes_for(const Geo& g, int B, int64_t G) {
   return ws_counters(g) + ws_partials(g, B, G) + ws_tiles(g, B) + ws_sums(g, B) + ws_xpad(g, B);
 }
 
-template <int BITS, int NN, int DWG>
+template <int BITS, int NN, int DWG, bool GRP = false>
 static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
-  using C = Cfg<BITS, NN, DWG>;
+  using C = Cfg<BITS, NN, DWG, GRP>;
   Params p = p0;
   const int64_t tile_bytes = (int64_t)NN * kSuperStep;
   int dev = 0, maxsmem = 0;
@@ -1430,7 +1437,7 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   if (nst < 2) return OWQ_ERR_UNSUPPORTED;     // too many weak columns / batch rows for shared memory
   p.nst = nst;
   const size_t smem = (size_t)nst * p.stage_bytes + fixed + (size_t)nst * 32;
-  auto kern = owq_gemv_kernel<BITS, NN, DWG>;
+  auto kern = owq_gemv_kernel<BITS, NN, DWG, GRP>;
   static thread_local size_t configured = 0;
   if (configured < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -1465,6 +1472,7 @@ static owq_status launch_n(const Params& p, int64_t grid, cudaStream_t cs) {
     case 8:   // batch 1: 2 decode warpgroups x 6 items measured best (fewer TMEM stores racing the MMAs)
       if (dwg == 3) return launch<BITS, 8, 3>(p, grid, cs);
       if (dwg == 4) return launch<BITS, 8, 4>(p, grid, cs);
+      if (p.g.group) return launch<BITS, 8, 2, true>(p, grid, cs);   // grouped scales: per-stage D blocks
       return launch<BITS, 8, 2>(p, grid, cs);
     case 16: return launch<BITS, 16, 3>(p, grid, cs);
     case 32: return launch<BITS, 32, 3>(p, grid, cs);
