@@ -763,21 +763,17 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       ++dcnt;
       open = false;
     };
-    StageIter it;
-    it.init(g, i0, i1, p.cap);
-    auto next_code = [&](int64_t& rb_, int32_t& li_) {
-      int32_t m;
-      while ((m = it.next(rb_, li_)) > 0 && li_ >= g.nss) {}
-      return m;
-    };
-    int64_t srb, nrb = -1;
-    int32_t sli, nli = 0;
-    int32_t n = next_code(srb, sli);
+    // The stage sequence comes from the producer's descriptors (desc[s], visible
+    // once full[s] completed; a descriptor with n == 0 ends the sequence).
     int j = 0, kst = 0;
-    while (n > 0) {
-      const int32_t nn = next_code(nrb, nli);
-      const uint32_t buf = (uint32_t)j & 1u;
+    for (;;) {
       const int s = j % NST;
+      mbar_wait(&full[s], (uint32_t)(j / NST) & 1u);
+      const StageDesc dsc = load_desc(&desc[s]);
+      if (dsc.n == 0) break;
+      const int64_t srb = dsc.rb;
+      const int32_t sli = dsc.li, n = dsc.n;
+      const uint32_t buf = (uint32_t)j & 1u;
       if (ISS == 1 || (int)buf == ii) {
         const long long t0 = clock64();
         mbar_wait(&afull[wg * 2 + buf], ((uint32_t)j >> 1) & 1u);
@@ -790,7 +786,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
         if (p.trace && dq == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
         tc_fence_after();
         const uint32_t stile = ring0 + (uint32_t)s * (uint32_t)p.stage_bytes;
-        const bool cont = nn > 0 && nrb == srb && ((nli >> gl) == ((sli + n - 1) >> gl));   // last group continues
+        const bool cont = (dsc.flags & kGroupCont) != 0;   // the stage's last group continues in the next stage
         if (C::kGP > 1 && p.g.group) {
           // grouped scales: D of this stage = [buf][piece] blocks, drained by the
           // epilogue per stage (dempty of the stage that used this buffer before)
@@ -865,15 +861,11 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           ends = true;   // (defensive: the group ended before this stage)
         } else {
           const bool later = ((sli + n - 1) >> gl) != ogi;   // the stage reaches a later group
-          const bool cont = nn > 0 && nrb == srb && (nli >> gl) == ogi;
-          ends = later || !cont;
+          ends = later || !(dsc.flags & kGroupCont);
         }
         if (ends) close_group();
       }
       ++j;
-      srb = nrb;
-      sli = nli;
-      n = nn;
     }
     if (open && !(C::kGP > 1 && p.g.group)) close_group();
     if (p.trace && lane == 0) {
