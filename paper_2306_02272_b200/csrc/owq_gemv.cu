@@ -81,6 +81,9 @@ struct Params {
   int32_t group_log2;     // log2(group_size / 64)
   int32_t span[kMaxGrid + 1];  // first item of each CTA (stream-K split, host-computed)
   int32_t coresident;          // grid <= SM count: fixed summer per row-block (see the fixup)
+  // per CTA: the CTAs holding the first / last item of the row-block of its first
+  // item (bits 0-15 / 16-31) and of its last item (bits 32-47 / 48-63)
+  uint64_t fix[kMaxGrid];
   unsigned long long* trace;   // experiments only (OWQ_TRACE)
   int32_t exp;                 // experiments only (OWQ_EXP): 3 = skip the TMEM stores
 };
@@ -497,6 +500,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
   int64_t* span = reinterpret_cast<int64_t*>(mbox + 2 * DWG);         // [2] this CTA's item range
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(span + 2);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* pubbar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(flag + 1) + 7) & ~(uintptr_t)7);
 
   const int64_t grid = gridDim.x, cta = blockIdx.x;
   if (threadIdx.x == 0) {
@@ -510,6 +514,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
     }
     for (int i = 0; i < 2 * DWG; ++i) { mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); }
     for (int i = 0; i < 2 * NDQ; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
+    mbar_init(pubbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == C::kProdWarp) {
@@ -522,6 +527,11 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t i0 = span[0], i1 = span[1];
+  if (p.trace && threadIdx.x == 0) {
+    p.trace[cta * 256 + 58] = (unsigned long long)i0;
+    p.trace[cta * 256 + 59] = (unsigned long long)i1;
+    p.trace[cta * 256 + 61] = (unsigned long long)items_per_rb(g);
+  }
   const int n_rb = items_per_rb(g);
   const uint32_t tile_bytes = (uint32_t)NN * kSuperStep;
 
@@ -621,6 +631,14 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       if (k >= NST) mbar_wait(&empty[s], ph ^ 1u);
       asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(smem_addr(&desc[s])), "r"(0u) : "memory");
       mbar_arrive(&full[s]);
+      // Publication of this CTA's piece of its first row-block when another CTA
+      // sums that row-block (co-resident grids): the epilogue stores the partial
+      // and arrives on pubbar; this thread, idle by now, makes it visible with a
+      // release add so the epilogue never stalls on the release fence.
+      if (p.coresident && i1 > i0 && i0 % n_rb != 0) {
+        mbar_wait(pubbar, 0u);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + i0 / n_rb) : "memory");
+      }
     }
   } else if (warp < C::kDecodeWarps) {
     // ==================================================================== decode
@@ -912,13 +930,14 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
     uint4 wpre[2];                                       // this row's first two weak chunks of the row-block (prefetch)
     int64_t wpre_rb = -1;
     int ngend = 0, kst = 0, rr = 0;
-    auto cta_of = [&](int64_t item) {   // span table search: span[c] <= item < span[c + 1]
-      int lo_c = 0, hi_c = (int)grid;
-      while (hi_c - lo_c > 1) {
-        const int mid = (lo_c + hi_c) >> 1;
-        if (p.span[mid] <= item) lo_c = mid; else hi_c = mid;
-      }
-      return (int64_t)lo_c;
+    // pieces of this CTA's first and last row-block (host table; the row-blocks
+    // in between are whole in this CTA)
+    const int64_t rb_a = i0 / n_rb, rb_b = (i1 - 1) / n_rb;
+    const uint64_t fx = p.fix[cta];
+    auto pieces = [&](int64_t rb, int64_t& cf, int64_t& cl) {
+      if (rb == rb_a) { cf = (int64_t)(fx & 0xFFFF); cl = (int64_t)((fx >> 16) & 0xFFFF); }
+      else if (rb == rb_b) { cf = (int64_t)((fx >> 32) & 0xFFFF); cl = (int64_t)(fx >> 48); }
+      else { cf = cta; cl = cta; }
     };
     // Early fixup of the summer (co-resident grids, batch <= 2): the other pieces of
     // a row-block stored their partials long before the summer reaches it, so the
@@ -1076,7 +1095,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
             const int64_t cend_e = (i1 - crb * n_rb < (int64_t)g.nss ? i1 - crb * n_rb : (int64_t)g.nss) - 1;
             if (MAXB <= 2 && p.coresident && cli + pb == cend_e && pre_rb != crb && crb * n_rb >= i0 &&
                 crb * n_rb + n_rb - 1 >= i1) {
-              const int64_t c_last = cta_of(crb * n_rb + n_rb - 1);
+              int64_t c_first_, c_last;
+              pieces(crb, c_first_, c_last);
               const int npieces = (int)(c_last - cta + 1);
               if (npieces - 1 <= kPreMax) {
                 if (et == 0) {
@@ -1223,7 +1243,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           for (int b = 0; b < MAXB; ++b)
             if (b < p.B) __stcg(&p.partial[((crb + cta) * p.B + b) * kRowBlock + row], tot[b]);
           // pieces = CTAs holding the first .. last item of the row-block (none is empty)
-          const int64_t c_first = cta_of(ifirst), c_last = cta_of(ilast);
+          int64_t c_first, c_last;
+          pieces(crb, c_first, c_last);
           const int npieces = (int)(c_last - c_first + 1);
           named_sync(2, 128);
           if (MAXB <= 2 && pre_rb == crb) {
@@ -1246,7 +1267,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
             // the row-block last).  Other pieces publish with a release add (only
             // that thread waits for its release fence) and go on; the summer
             // acquires the count, then sums all pieces in a fixed order.
-            if (et == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + crb) : "memory");
+            // (always this CTA's first row-block: the producer thread publishes it)
+            if (et == 0) mbar_arrive(pubbar);
           } else {
           if (p.coresident) {
             {
@@ -1397,6 +1419,9 @@ static size_t ws_bytes_for(const Geo& g, int B, int64_t G) {
   return ws_counters(g) + ws_partials(g, B, G) + ws_tiles(g, B) + ws_sums(g, B) + ws_xpad(g, B);
 }
 
+static unsigned long long* g_trace_buf = nullptr;   // experiments only (OWQ_TRACE)
+static int64_t g_trace_grid = 0;
+
 template <int BITS, int NN, int DWG, bool GRP = false>
 static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   using C = Cfg<BITS, NN, DWG, GRP>;
@@ -1495,6 +1520,24 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.sums = sums;
   p.g = g;
   for (int64_t c = 0; c <= grid; ++c) p.span[c] = (int32_t)cta_first_item(g, grid, c);
+  {  // row-block pieces at each CTA's ends (the fixup's summer and piece count)
+    const int64_t n_rb = items_per_rb(g);
+    auto cta_of = [&](int64_t item) {   // span[c] <= item < span[c + 1]
+      int64_t lo = 0, hi = grid;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (p.span[mid] <= item) lo = mid; else hi = mid;
+      }
+      return (uint64_t)lo;
+    };
+    for (int64_t c = 0; c < grid; ++c) {
+      const int64_t i0 = p.span[c], i1 = p.span[c + 1];
+      if (i1 <= i0) { p.fix[c] = (uint64_t)c * 0x0001000100010001ull; continue; }
+      const int64_t ra = i0 / n_rb, rbb = (i1 - 1) / n_rb;
+      p.fix[c] = cta_of(ra * n_rb) | (cta_of(ra * n_rb + n_rb - 1) << 16) | (cta_of(rbb * n_rb) << 32) |
+                 (cta_of(rbb * n_rb + n_rb - 1) << 48);
+    }
+  }
   p.coresident = grid <= device_sms() ? 1 : 0;   // one CTA per SM: every CTA is resident at once
   p.B = B;
   p.Bp = batch_pad(B);
@@ -1528,13 +1571,22 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
                        mma_n_for(B), tiles, (long long*)sums);
     if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
   }
-  static unsigned long long* trace_buf = nullptr;
+  // experiments only: OWQ_TRACE=<file> appends each call's per-CTA stamps to the
+  // file; with OWQ_TRACE_DEFER set, calls only record (graph-capturable) and
+  // owq_debug_trace_dump() writes the last launch's stamps.
   static const char* trace_path = getenv("OWQ_TRACE");
-  if (trace_path && !trace_buf) cudaMalloc(&trace_buf, 4096 * 256 * 8);
+  static const bool trace_defer = getenv("OWQ_TRACE_DEFER") != nullptr;
+  if (trace_path && !g_trace_buf) {
+    cudaMalloc(&g_trace_buf, 4096 * 256 * 8);
+    cudaMemset(g_trace_buf, 0, 4096 * 256 * 8);
+  }
+  unsigned long long* trace_buf = trace_defer ? nullptr : g_trace_buf;
   if (trace_buf) cudaMemsetAsync(trace_buf, 0, 4096 * 256 * 8, cs);
-  p.trace = trace_buf;
+  p.trace = g_trace_buf;
+  g_trace_grid = grid;
   static const int exp_env = getenv("OWQ_EXP") ? atoi(getenv("OWQ_EXP")) : 0;
   p.exp = exp_env;
+
   p.group_log2 = 0;
   if (g.group) while ((kSuperStep << p.group_log2) < g.group) ++p.group_log2;
   const owq_status rs = skip == 2 ? OWQ_OK : (g.bits == 3 ? launch_n<3>(p, grid, cs) : launch_n<4>(p, grid, cs));
@@ -1548,6 +1600,20 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
 }
 
 }  // namespace owq
+
+// experiments only (not part of the C ABI in include/owq.h): write the stamps
+// of the last traced launch (OWQ_TRACE + OWQ_TRACE_DEFER) to `path`.
+extern "C" int owq_debug_trace_dump(const char* path) {
+  if (!owq::g_trace_buf) return -1;
+  std::vector<unsigned long long> h((size_t)owq::g_trace_grid * 256);
+  if (cudaDeviceSynchronize() != cudaSuccess) return -2;
+  cudaMemcpy(h.data(), owq::g_trace_buf, h.size() * 8, cudaMemcpyDeviceToHost);
+  FILE* f = fopen(path, "wb");
+  if (!f) return -3;
+  fwrite(h.data(), 8, h.size(), f);
+  fclose(f);
+  return 0;
+}
 
 using namespace owq;
 
