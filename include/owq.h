@@ -130,11 +130,14 @@ owq_status owq_blob_decode_host(const void *h_blob, size_t blob_bytes,
 owq_status owq_unpack_codes(const owq_shape *shape, const void *d_packed,
                             uint8_t *d_codes, void *stream);
 
-/* Workspace of owq_gemv / owq_gemm_small_batch on the current device:
- * per-row-block stream-K arrival counters, fp32 partial sums, and the exact
- * int8 digit tiles + int64 digit sums of x written by each call's x pass.
- * The caller zero-fills it ONCE; every call leaves the counters at zero again.
- * One workspace must not be used by two calls that may run concurrently. */
+/* Workspace of owq_gemv / owq_gemm_small_batch on the current device: a fixed
+ * 4 MiB prefix of stream-K partial-row slots (one per CTA and batch row; a zero
+ * word means "not written yet"), per-row-block arrival counters and fp32
+ * partials for grids larger than the SM count, and the exact int8 digit tiles +
+ * int64 digit sums of x written by each call's x pass.  The caller zero-fills
+ * it ONCE; every call leaves the slots at zero again, so one workspace (sized
+ * for the largest shape) serves sequential calls of any shapes.  One workspace
+ * must not be used by two calls that may run concurrently. */
 size_t owq_workspace_bytes(const owq_shape *shape, int batch);
 
 /* y = W_hat x for one activation vector (batch 1).

@@ -62,6 +62,7 @@ struct Params {
   const __half* x;
   void* y;
   uint32_t* counters;
+  uint32_t* slots;        // co-resident fixup: [cta][B][128] partial rows as ~bits (0 = not written)
   float* partial;
   const uint8_t* tiles;   // x digits, [nss][NN rows x 64 columns] in UMMA K-major core matrices
   const long long* sums;  // [nss][Bp] sum over the super-step of x * 2^24
@@ -98,6 +99,14 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* a) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* a, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -311,15 +320,23 @@ __device__ __forceinline__ void decode_row(const uint32_t* w, uint32_t* o, const
 // row n = 8 nb + r (= 6 b + i; rows >= 6 B are zero), column k = 16 kc + kk of the
 // super-step.  sums: [nss][Bp] = sum over the super-step's columns of x * 2^24.
 __device__ __forceinline__ long long x_fixed(__half h) { return (long long)(__half2float(h) * 16777216.0f); }
+// The pass also zeroes the GEMV's synchronisation words (stream-K counters and
+// partial rows, `nzero` 16-byte words at `zero`): the GEMV's fixup treats a zero
+// partial word as "not written yet", and a workspace shared by calls of other
+// shapes holds their tiles / sums there.  CTAs past nss only zero.
 __global__ void owq_x_digits_kernel(const __half* __restrict__ x, int64_t xK, int B, int Bp, int K, int NN,
-                                    uint8_t* __restrict__ tiles, long long* __restrict__ sums) {
+                                    uint8_t* __restrict__ tiles, long long* __restrict__ sums, int nss,
+                                    uint4* __restrict__ zero, int64_t nzero) {
   __shared__ long long part[2 * OWQ_MAX_BATCH];
   // Let the GEMV start (prologue, weight prefetch, decode) as soon as SMs free up,
   // even before the previous GEMV has finished; everything it reads that depends on
   // earlier kernels (x, digit tiles / sums, workspace) is behind its own pdl_wait().
   pdl_launch_dependents();
   pdl_wait();                  // x and the workspace belong to earlier kernels until they complete
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nzero; i += (int64_t)gridDim.x * blockDim.x)
+    zero[i] = make_uint4(0, 0, 0, 0);
   const int ss = blockIdx.x;
+  if (ss >= nss) return;
   const int b = threadIdx.x >> 6, k = threadIdx.x & 63;   // blockDim = 64 * Bp
   const int nbk = NN / 8;
   const int64_t col = (int64_t)ss * kSuperStep + k;
@@ -500,7 +517,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
   int64_t* span = reinterpret_cast<int64_t*>(mbox + 2 * DWG);         // [2] this CTA's item range
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(span + 2);
   int* flag = reinterpret_cast<int*>(tmem_slot + 1);
-  uint64_t* pubbar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(flag + 1) + 7) & ~(uintptr_t)7);
 
   const int64_t grid = gridDim.x, cta = blockIdx.x;
   if (threadIdx.x == 0) {
@@ -514,7 +530,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
     }
     for (int i = 0; i < 2 * DWG; ++i) { mbar_init(&afull[i], 4); mbar_init(&aempty[i], 1); }
     for (int i = 0; i < 2 * NDQ; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 4); }
-    mbar_init(pubbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == C::kProdWarp) {
@@ -631,14 +646,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       if (k >= NST) mbar_wait(&empty[s], ph ^ 1u);
       asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(smem_addr(&desc[s])), "r"(0u) : "memory");
       mbar_arrive(&full[s]);
-      // Publication of this CTA's piece of its first row-block when another CTA
-      // sums that row-block (co-resident grids): the epilogue stores the partial
-      // and arrives on pubbar; this thread, idle by now, makes it visible with a
-      // release add so the epilogue never stalls on the release fence.
-      if (p.coresident && i1 > i0 && i0 % n_rb != 0) {
-        mbar_wait(pubbar, 0u);
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.counters + i0 / n_rb) : "memory");
-      }
     }
   } else if (warp < C::kDecodeWarps) {
     // ==================================================================== decode
@@ -939,13 +946,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       else if (rb == rb_b) { cf = (int64_t)((fx >> 32) & 0xFFFF); cl = (int64_t)(fx >> 48); }
       else { cf = cta; cl = cta; }
     };
-    // Early fixup of the summer (co-resident grids, batch <= 2): the other pieces of
-    // a row-block stored their partials long before the summer reaches it, so the
-    // summer checks the count when it opens its last group of that row-block and,
-    // if complete, loads their partials then; at the finish it only adds them.
-    constexpr int kPreMax = 8;
-    float pre[MAXB <= 2 ? MAXB : 1][kPreMax];
-    int64_t pre_rb = -1;
     StageIter it;
     it.init(g, i0, i1, p.cap);
     int64_t crb, nrb = -1;
@@ -1090,33 +1090,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           }
           if (ends) {
             if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 18 + 6 * ngend] = gtime();
-            // summer of a split row-block, last group: acquire the other pieces' count
-            // and load their partials now, while the pipeline drains this group
-            const int64_t cend_e = (i1 - crb * n_rb < (int64_t)g.nss ? i1 - crb * n_rb : (int64_t)g.nss) - 1;
-            if (MAXB <= 2 && p.coresident && cli + pb == cend_e && pre_rb != crb && crb * n_rb >= i0 &&
-                crb * n_rb + n_rb - 1 >= i1) {
-              int64_t c_first_, c_last;
-              pieces(crb, c_first_, c_last);
-              const int npieces = (int)(c_last - cta + 1);
-              if (npieces - 1 <= kPreMax) {
-                if (et == 0) {
-                  unsigned c;
-                  for (;;) {
-                    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(p.counters + crb) : "memory");
-                    if (c == (unsigned)(npieces - 1)) break;
-                    __nanosleep(100);
-                  }
-                }
-                named_sync(2, 128);
-                pre_rb = crb;
-#pragma unroll
-                for (int b = 0; b < (MAXB <= 2 ? MAXB : 1); ++b)
-#pragma unroll
-                  for (int qq = 0; qq < kPreMax; ++qq)
-                    pre[b][qq] = (b < p.B && qq < npieces - 1)
-                                     ? __ldcg(&p.partial[((crb + cta + 1 + qq) * p.B + b) * kRowBlock + row]) : 0.f;
-              }
-            }
             // block-reduce the digit-sum shares (the same for every row)
             long long S[MAXB];
             long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
@@ -1239,70 +1212,80 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
               }
           }
         } else {
-#pragma unroll
-          for (int b = 0; b < MAXB; ++b)
-            if (b < p.B) __stcg(&p.partial[((crb + cta) * p.B + b) * kRowBlock + row], tot[b]);
           // pieces = CTAs holding the first .. last item of the row-block (none is empty)
           int64_t c_first, c_last;
           pieces(crb, c_first, c_last);
           const int npieces = (int)(c_last - c_first + 1);
-          named_sync(2, 128);
-          if (MAXB <= 2 && pre_rb == crb) {
-            // summer with the other pieces prefetched: fixed-order sum, no round trip
-            if (et == 0) p.counters[crb] = 0u;
-            if (grow < g.M) {
+          uint32_t* pw = p.slots;   // [cta][B][128]: each CTA has at most one non-summer piece (its first row-block)
+          if (p.coresident) {
+            // Fixed summer = the CTA holding the row-block's first item (it reaches
+            // the row-block last).  The other pieces store their partial rows as
+            // ~bits (a zero word = not written yet: the workspace starts zeroed and
+            // the summer zeroes what it consumed), so each summer thread polls its
+            // own rows' words -- no fences, counters or barriers -- and adds the
+            // pieces in a fixed order.
+            if (cta != c_first) {
 #pragma unroll
-              for (int b = 0; b < (MAXB <= 2 ? MAXB : 1); ++b)
-                if (b < p.B) {
-                  float v = tot[b];
+              for (int b = 0; b < MAXB; ++b)
+                if (b < p.B) st_relaxed(pw + (cta * p.B + b) * kRowBlock + row, ~__float_as_uint(tot[b]));
+            } else {
+              for (int qq = 1; qq < npieces; ++qq) {
+                // all batch rows of piece qq in flight at once, then wait for the late ones
+                uint32_t w[MAXB];
 #pragma unroll
-                  for (int qq = 0; qq < kPreMax; ++qq)
-                    if (qq < npieces - 1) v += pre[b][qq];
+                for (int b = 0; b < MAXB; ++b)
+                  w[b] = b < p.B ? ld_relaxed(pw + ((c_first + qq) * p.B + b) * kRowBlock + row) : 1u;
+#pragma unroll
+                for (int b = 0; b < MAXB; ++b)
+                  if (b < p.B) {
+                    uint32_t* a = pw + ((c_first + qq) * p.B + b) * kRowBlock + row;
+                    while (w[b] == 0u) {
+                      __nanosleep(32);
+                      w[b] = ld_relaxed(a);
+                    }
+                    st_relaxed(a, 0u);
+                    tot[b] += __uint_as_float(~w[b]);
+                  }
+              }
+              if (grow < g.M) {
+#pragma unroll
+                for (int b = 0; b < MAXB; ++b)
+                  if (b < p.B) {
+                    if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = tot[b];
+                    else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(tot[b]);
+                  }
+              }
+            }
+          } else {
+            // grids larger than the SM count: the last piece to arrive sums (acq_rel
+            // counter; the x pass zeroes the counters)
+#pragma unroll
+            for (int b = 0; b < MAXB; ++b)
+              if (b < p.B) __stcg(&p.partial[((crb + cta) * p.B + b) * kRowBlock + row], tot[b]);
+            named_sync(2, 128);
+            if (et == 0) {
+              // releases this CTA's partial stores (ordered before by the barrier),
+              // acquires the other pieces' stores when we are last
+              unsigned old;
+              asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counters + crb) : "memory");
+              const int last = old == (unsigned)(npieces - 1);
+              if (last) p.counters[crb] = 0u;   // all pieces arrived: reset for the next call
+              *flag = last;
+            }
+            named_sync(2, 128);
+            if (*flag) {
+              for (int b = 0; b < p.B; ++b) {
+                float v = 0.f;
+                for (int qq = 0; qq < npieces; ++qq) {
+                  v += __ldcg(&p.partial[((crb + c_first + qq) * p.B + b) * kRowBlock + row]);
+                }
+                if (grow < g.M) {
                   if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = v;
                   else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(v);
                 }
-            }
-          } else if (p.coresident && cta != c_first) {
-            // Fixed summer = the CTA holding the row-block's first item (it reaches
-            // the row-block last).  Other pieces publish with a release add (only
-            // that thread waits for its release fence) and go on; the summer
-            // acquires the count, then sums all pieces in a fixed order.
-            // (always this CTA's first row-block: the producer thread publishes it)
-            if (et == 0) mbar_arrive(pubbar);
-          } else {
-          if (p.coresident) {
-            {
-              if (et == 0) {
-                unsigned c;
-                for (;;) {
-                  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(p.counters + crb) : "memory");
-                  if (c == (unsigned)(npieces - 1)) break;
-                  __nanosleep(200);
-                }
-                p.counters[crb] = 0u;   // reset for the next call
               }
-              *flag = 1;
             }
-          } else if (et == 0) {
-            // acq_rel: releases this CTA's partial stores (ordered before by the
-            // barrier), acquires the other pieces' stores when we are last
-            unsigned old;
-            asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counters + crb) : "memory");
-            const int last = old == (unsigned)(npieces - 1);
-            if (last) p.counters[crb] = 0u;   // all pieces arrived: reset for the next call
-            *flag = last;
-          }
-          named_sync(2, 128);
-          if (*flag && grow < g.M) {
-            for (int b = 0; b < p.B; ++b) {
-              float v = 0.f;
-              for (int qq = 0; qq < npieces; ++qq)
-                v += __ldcg(&p.partial[((crb + c_first + qq) * p.B + b) * kRowBlock + row]);
-              if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = v;
-              else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(v);
-            }
-          }
-          named_sync(2, 128);
+            named_sync(2, 128);
           }
         }
 #pragma unroll
@@ -1408,6 +1391,10 @@ static owq_status check_blob_cached(const owq_shape* s, const void* d_packed, Ge
 
 // Workspace: [counters nrb u32][partials (nrb + grid) x B x 128 f32]
 //            [x digit tiles nss x NN x 64 B][x digit sums nss x Bp x 8 B]
+// Fixed-size prefix shared by every shape: one partial-row slot per (CTA, batch
+// row) for the co-resident fixup's zero-word protocol (zero = not written yet;
+// every call leaves it zero), so calls of other shapes never put data there.
+static size_t ws_sync() { return (size_t)kMaxGrid * OWQ_MAX_BATCH * kRowBlock * 4; }
 static size_t ws_counters(const Geo& g) { return ((size_t)g.nrb * 4 + 255) / 256 * 256; }
 static size_t ws_partials(const Geo& g, int B, int64_t G) {
   return ((size_t)(g.nrb + G) * B * kRowBlock * 4 + 255) / 256 * 256;
@@ -1416,7 +1403,7 @@ static size_t ws_tiles(const Geo& g, int B) { return (size_t)g.nss * mma_n_for(B
 static size_t ws_sums(const Geo& g, int B) { return (size_t)g.nss * batch_pad(B) * 8; }
 static size_t ws_xpad(const Geo& g, int B) { return ((size_t)B * g.nss * kSuperStep * 2 + 255) / 256 * 256; }
 static size_t ws_bytes_for(const Geo& g, int B, int64_t G) {
-  return ws_counters(g) + ws_partials(g, B, G) + ws_tiles(g, B) + ws_sums(g, B) + ws_xpad(g, B);
+  return ws_sync() + ws_counters(g) + ws_partials(g, B, G) + ws_tiles(g, B) + ws_sums(g, B) + ws_xpad(g, B);
 }
 
 static unsigned long long* g_trace_buf = nullptr;   // experiments only (OWQ_TRACE)
@@ -1512,9 +1499,10 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.blob = (const uint8_t*)d_packed;
   p.x = (const __half*)d_x;
   p.y = d_y;
-  p.counters = (uint32_t*)d_ws;
-  p.partial = (float*)((uint8_t*)d_ws + ws_counters(g));
-  uint8_t* tiles = (uint8_t*)d_ws + ws_counters(g) + ws_partials(g, B, grid);
+  p.slots = (uint32_t*)d_ws;
+  p.counters = (uint32_t*)((uint8_t*)d_ws + ws_sync());
+  p.partial = (float*)((uint8_t*)d_ws + ws_sync() + ws_counters(g));
+  uint8_t* tiles = (uint8_t*)d_ws + ws_sync() + ws_counters(g) + ws_partials(g, B, grid);
   long long* sums = (long long*)(tiles + ws_tiles(g, B));
   p.tiles = tiles;
   p.sums = sums;
@@ -1546,7 +1534,7 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   cudaStream_t cs = (cudaStream_t)stream;
   if (false) {   // in-kernel digit mode only (off): TMA of x needs 16-byte aligned rows
     // in-kernel digit mode streams x with TMA: rows must be 16-byte aligned
-    __half* xp = (__half*)((uint8_t*)d_ws + ws_counters(g) + ws_partials(g, B, grid) + ws_tiles(g, B) + ws_sums(g, B));
+    __half* xp = (__half*)((uint8_t*)d_ws + ws_sync() + ws_counters(g) + ws_partials(g, B, grid) + ws_tiles(g, B) + ws_sums(g, B));
     const int Kp = g.nss * kSuperStep;
     const int64_t n = (int64_t)B * Kp;
     owq_pad_x_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, cs>>>(p.x, xp, B, g.K, Kp);
@@ -1562,13 +1550,16 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl >= 2 ? 1 : 0;
-    cfg.gridDim = dim3((unsigned)g.nss);
+    // the stream-K counters (used by grids larger than the SM count) start at zero
+    const int64_t nzero = grid > device_sms() ? (int64_t)ws_counters(g) / 16 : 0;
+    const int64_t zctas = (nzero + 1023) / 1024;
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(g.nss, std::min<int64_t>(zctas, 1024)));
     cfg.blockDim = dim3((unsigned)(64 * p.Bp));
     cfg.stream = cs;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, owq_x_digits_kernel, (const __half*)p.x, (int64_t)p.xK, B, (int)p.Bp, (int)g.K,
-                       mma_n_for(B), tiles, (long long*)sums);
+                       mma_n_for(B), tiles, (long long*)sums, (int)g.nss, (uint4*)p.counters, nzero);
     if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
   }
   // experiments only: OWQ_TRACE=<file> appends each call's per-CTA stamps to the
