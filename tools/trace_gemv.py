@@ -72,4 +72,4 @@ if t[:, 61].max() > 0:
     print(" fastest / slowest CTAs: idx start end dur | parts (W whole rb, S summer piece, p other piece, items)")
     for c in list(order[:5]) + list(order[-6:]):
         print(f"   {c:4d} {st[c]:6.2f} {en[c]:6.2f} {du[c]:6.2f} | {role(c):24s} fin-in {rel(t[c,50]):6.2f} fin-out {rel(t[c,56]):6.2f}"
-              f"  last group [seen, S, D, comb] " + str([round(rel(t[c, 18 + 6 * j + i]), 2) for j in range(4) for i in range(4) if t[c, 18 + 6 * j] > 0][-4:]))
+              f" fin1 {rel(t[c,51]):6.2f}-{rel(t[c,60]):6.2f} open2 {rel(t[c,17]) if t[c,17] else -1:6.2f} groups [seen, S, D, comb] " + str([round(rel(t[c, 18 + 6 * j + i]), 2) for j in range(4) for i in range(4) if t[c, 18 + 6 * j] > 0][-8:]))
