@@ -237,7 +237,8 @@ def owq_workspace_bytes(shape, batch: int = 1) -> int:
 
 
 def workspace(shape, batch: int = 1, device=None, grid: int = 0):
-    """Zero-filled workspace (counters stay zero between calls)."""
+    """Zero-filled workspace (every call leaves its stream-K slots and counters
+    at zero again, so one workspace serves sequential calls of any shapes)."""
     import torch
     n = owq_workspace_bytes(shape, batch)
     if grid:   # stream-K partial slots for a non-default grid: grid x batch x 128 rows x f32

@@ -280,3 +280,38 @@ def test_concurrent_streams_partial_grids(dev):
     for r in runs:
         e, _ = rel_err(r["y"].cpu().numpy().astype(np.float64), r["ref"])
         assert e <= TOL
+
+
+def test_workspace_sync_words_left_zero(dev):
+    """One workspace shared by calls of different shapes, batches and grids --
+    co-resident (zero-word slot protocol) and larger than the SM count (counter
+    protocol) -- in one stream with no synchronisation in between: every output
+    matches the oracle and the fixed synchronisation prefix of the workspace
+    (partial-row slots, 0 = not written) is all zero afterwards."""
+    cases = [(1000, 700, 3, 0, 11, 1, 0), (4096, 2048, 3, 0, 9, 2, 500), (300, 2000, 4, 128, 7, 1, 0),
+             (2048, 4096, 4, 0, 3, 8, 0), (768, 768, 3, 0, 8, 1, 300), (4096, 1024, 3, 0, 5, 3, 0)]
+    layers, xs, refs, ws_bytes = [], [], [], 0
+    for i, (M, K, bits, g, k, B, grid) in enumerate(cases):
+        d = synth.representation(M, K, bits, g, k, seed=300 + i)
+        x = synth.activations(B, K, seed=400 + i, outliers=d["weak_idx"][:4])
+        L = owq.OwqLinear(d, device=dev)
+        layers.append((L, grid))
+        xs.append(torch.from_numpy(x).to(dev))
+        refs.append(O.matvec(rep_from_synth(d), x.astype(np.float64)))
+        ws_bytes = max(ws_bytes, owq.workspace(L.shape, B, dev, grid=grid).numel())
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
+    for _ in range(2):
+        ys = []
+        for (L, grid), x in zip(layers, xs):
+            y = torch.empty((x.shape[0], L.shape.c_out), dtype=torch.float32, device=dev)
+            if grid:
+                owq.owq_gemm_small_batch_grid(L.shape, L.packed, x, grid, y=y, y_f32=True, ws=ws)
+            else:
+                owq.owq_gemm_small_batch(L.shape, L.packed, x, y=y, y_f32=True, ws=ws)
+            ys.append(y)
+        torch.cuda.synchronize()
+        for y, ref in zip(ys, refs):
+            e, _ = rel_err(y.cpu().numpy().astype(np.float64), ref)
+            assert e <= TOL
+        slots = 512 * 16 * 128 * 4   # kMaxGrid x OWQ_MAX_BATCH x 128 rows x 4 B (owq_gemv.cu ws_sync)
+        assert int(torch.count_nonzero(ws[:slots]).item()) == 0
