@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
     gm_g = -1;                                                                                          \
   } while (0)
     while (cn > 0) {
-      const int32_t nn = it.next(nrb, nli);
+      int32_t nn = it.next(nrb, nli);
       if (cli < g.nss && gmode) {
         // one D buffer per stage and warpgroup: [piece] blocks of kGP x NN columns
         const int gA = cli >> gl;
@@ -1150,6 +1150,23 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           pa = pb + 1;
         }
         ++jc;
+        if (!g.group && C::ISS == 1 && gopen) {
+          // Per-row scales: the stages between a group's first and last one need
+          // nothing from the epilogue (they are full, so every warpgroup has
+          // items) -- jump the walk to the group's last stage.
+          const int64_t rb0 = crb * n_rb;
+          const int64_t gs = i0 > rb0 ? i0 - rb0 : 0;                                  // group start (rb-relative)
+          const int64_t ge = i1 - rb0 < (int64_t)g.nss ? i1 - rb0 : (int64_t)g.nss;   // group end
+          const int64_t last = gs + (ge - gs - 1) / p.cap * p.cap;                     // its last stage
+          if (last > (int64_t)cli + cn) {
+#pragma unroll
+            for (int w = 0; w < DWG; ++w) part |= 1u << w;
+            it.rb = crb;
+            it.li = (int32_t)last;
+            it.left = i1 - (rb0 + last);
+            nn = it.next(nrb, nli);
+          }
+        }
       } else {
         // weak chunks (straight from the blob, not through the ring): fp16 weak
         // columns x gathered activations, fp32 (unscaled)
