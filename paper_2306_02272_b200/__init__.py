@@ -140,6 +140,11 @@ def _ptr(a):
 def _stream(stream):
     import torch
     if stream is None:
+        # the current stream's raw handle without the Python Stream object
+        # (torch.cuda.current_stream() costs several microseconds per call)
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:
+            return raw(torch._C._cuda_getDevice())
         return torch.cuda.current_stream().cuda_stream
     if isinstance(stream, int):
         return stream

@@ -1524,23 +1524,50 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.tiles = tiles;
   p.sums = sums;
   p.g = g;
-  for (int64_t c = 0; c <= grid; ++c) p.span[c] = (int32_t)cta_first_item(g, grid, c);
-  {  // row-block pieces at each CTA's ends (the fixup's summer and piece count)
-    const int64_t n_rb = items_per_rb(g);
-    auto cta_of = [&](int64_t item) {   // span[c] <= item < span[c + 1]
-      int64_t lo = 0, hi = grid;
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (p.span[mid] <= item) lo = mid; else hi = mid;
-      }
-      return (uint64_t)lo;
+  {
+    // Stream-K span table and row-block piece table of this (geometry, grid): a
+    // few recent ones are kept per host thread (the tables are pure functions of
+    // them and cost microseconds to rebuild on every call).
+    struct SpanCache {
+      int64_t key[4];
+      int32_t span[kMaxGrid + 1];
+      uint64_t fix[kMaxGrid];
     };
-    for (int64_t c = 0; c < grid; ++c) {
-      const int64_t i0 = p.span[c], i1 = p.span[c + 1];
-      if (i1 <= i0) { p.fix[c] = (uint64_t)c * 0x0001000100010001ull; continue; }
-      const int64_t ra = i0 / n_rb, rbb = (i1 - 1) / n_rb;
-      p.fix[c] = cta_of(ra * n_rb) | (cta_of(ra * n_rb + n_rb - 1) << 16) | (cta_of(rbb * n_rb) << 32) |
-                 (cta_of(rbb * n_rb + n_rb - 1) << 48);
+    static thread_local SpanCache cache[8];
+    static thread_local int cache_n = 0, cache_next = 0;
+    const int64_t key[4] = {g.nrb, g.rb_bytes, ((int64_t)g.nss << 32) | (int64_t)g.kpad, ((int64_t)g.ss_bytes << 32) | grid};
+    int hit = -1;
+    for (int i = 0; i < cache_n && hit < 0; ++i)
+      if (!std::memcmp(cache[i].key, key, sizeof(key))) hit = i;
+    if (hit < 0) {
+      for (int64_t c = 0; c <= grid; ++c) p.span[c] = (int32_t)cta_first_item(g, grid, c);
+      {  // row-block pieces at each CTA's ends (the fixup's summer and piece count)
+        const int64_t n_rb = items_per_rb(g);
+        auto cta_of = [&](int64_t item) {   // span[c] <= item < span[c + 1]
+          int64_t lo = 0, hi = grid;
+          while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (p.span[mid] <= item) lo = mid; else hi = mid;
+          }
+          return (uint64_t)lo;
+        };
+        for (int64_t c = 0; c < grid; ++c) {
+          const int64_t i0 = p.span[c], i1 = p.span[c + 1];
+          if (i1 <= i0) { p.fix[c] = (uint64_t)c * 0x0001000100010001ull; continue; }
+          const int64_t ra = i0 / n_rb, rbb = (i1 - 1) / n_rb;
+          p.fix[c] = cta_of(ra * n_rb) | (cta_of(ra * n_rb + n_rb - 1) << 16) | (cta_of(rbb * n_rb) << 32) |
+                     (cta_of(rbb * n_rb + n_rb - 1) << 48);
+        }
+      }
+      hit = cache_next;
+      cache_next = (cache_next + 1) % 8;
+      if (cache_n < 8) ++cache_n;
+      std::memcpy(cache[hit].key, key, sizeof(key));
+      std::memcpy(cache[hit].span, p.span, sizeof(int32_t) * (grid + 1));
+      std::memcpy(cache[hit].fix, p.fix, sizeof(uint64_t) * grid);
+    } else {
+      std::memcpy(p.span, cache[hit].span, sizeof(int32_t) * (grid + 1));
+      std::memcpy(p.fix, cache[hit].fix, sizeof(uint64_t) * grid);
     }
   }
   p.coresident = grid <= device_sms() ? 1 : 0;   // one CTA per SM: every CTA is resident at once
