@@ -1015,6 +1015,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
 #pragma unroll
                   for (int i = 0; i < kDigits; ++i) v += (long long)(int)dd[ph2 * NN + i] << (8 * i);
                   long long sp = 0;
+#pragma unroll 1
                   for (int t = ia; t < ib; ++t) {
                     const uint2 sv = lds64(sb + (uint32_t)p.sum_off + (uint32_t)(t * p.Bp) * 8u);
                     sp += (long long)(((unsigned long long)sv.y << 32) | sv.x);
