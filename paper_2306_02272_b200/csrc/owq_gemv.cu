@@ -933,6 +933,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
     uint32_t part = 0;                                   // D owners (warpgroup, issuer) with items in the open group
     int jc = 0;                                          // code-stage index (stage j -> issuer j & 1 when ISS == 2)
     bool gopen = false;
+    bool sdirect = false;                                // the open group's digit sums are complete in sacc
     uint32_t szw = 0;                                    // the open group's (s, z) for this row
     uint4 wpre[2];                                       // this row's first two weak chunks of the row-block (prefetch)
     int64_t wpre_rb = -1;
@@ -1070,10 +1071,20 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
             const int gfirst = cli + pa;
             const int64_t cend = (i1 - crb * n_rb < (int64_t)g.nss ? i1 - crb * n_rb : (int64_t)g.nss) - 1;   // CTA's last code item in rb
             const int glast = (int)(((int64_t)((gi + 1) << gl) - 1 < cend) ? ((gi + 1) << gl) - 1 : cend);
-            for (int li = gfirst + et; li <= glast; li += 128)
+            if (g.group && (glast - gfirst + 1) * MAXB <= 32) {
+              // small group: every thread sums the whole group (no block reduction at its end)
+              sdirect = true;
+#pragma unroll 1
+              for (int li = gfirst; li <= glast; ++li)
 #pragma unroll
-              for (int b = 0; b < MAXB; ++b)
-                if (b < p.B) sacc[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
+                for (int b = 0; b < MAXB; ++b)
+                  if (b < p.B) sacc[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
+            } else {
+              for (int li = gfirst + et; li <= glast; li += 128)
+#pragma unroll
+                for (int b = 0; b < MAXB; ++b)
+                  if (b < p.B) sacc[b] += __ldg(&p.sums[(int64_t)li * p.Bp + b]);
+            }
           }
           {
             const int iss = ISS == 1 ? 0 : (jc & 1);
@@ -1093,20 +1104,26 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
             if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 18 + 6 * ngend] = gtime();
             // block-reduce the digit-sum shares (the same for every row)
             long long S[MAXB];
-            long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
+            if (sdirect) {
 #pragma unroll
-            for (int b = 0; b < MAXB; ++b) {
-              long long v = sacc[b];
-              sacc[b] = 0;
+              for (int b = 0; b < MAXB; ++b) { S[b] = sacc[b]; sacc[b] = 0; }
+              sdirect = false;
+            } else {
+              long long* rd = red + (rr & 1) * 4 * OWQ_MAX_BATCH;
 #pragma unroll
-              for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-              if (lane == 0) rd[q * OWQ_MAX_BATCH + b] = v;
+              for (int b = 0; b < MAXB; ++b) {
+                long long v = sacc[b];
+                sacc[b] = 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) rd[q * OWQ_MAX_BATCH + b] = v;
+              }
+              named_sync(2, 128);
+#pragma unroll
+              for (int b = 0; b < MAXB; ++b)
+                S[b] = rd[b] + rd[OWQ_MAX_BATCH + b] + rd[2 * OWQ_MAX_BATCH + b] + rd[3 * OWQ_MAX_BATCH + b];
+              ++rr;
             }
-            named_sync(2, 128);
-#pragma unroll
-            for (int b = 0; b < MAXB; ++b)
-              S[b] = rd[b] + rd[OWQ_MAX_BATCH + b] + rd[2 * OWQ_MAX_BATCH + b] + rd[3 * OWQ_MAX_BATCH + b];
-            ++rr;
             if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 19 + 6 * ngend] = gtime();
             const __half2 szv = u2h(szw);
             const float s_g = __low2float(szv);
