@@ -266,6 +266,14 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* d) {
       : "memory");
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tc_ld16_nowait(uint32_t taddr, uint32_t* d) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+        "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+      : "r"(taddr)
+      : "memory");
+}
 // UMMA shared-memory descriptor, K-major, no swizzle (SM100 version = 1)
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
@@ -1140,19 +1148,38 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
                 named_sync(2, 128);
                 tc_fence_after();
                 const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + dbuf) * C::kGP * NN);
+                constexpr int kL = (MAXB * kDigits + 15) / 16;
+                if (kL <= 2) {
+                  // small D: into registers, back to the MMA warp, then combine
+                  uint32_t dall[kL][16];
 #pragma unroll
-                for (int c16 = 0; c16 < (MAXB * kDigits + 15) / 16; ++c16) {
-                  uint32_t dd[16];
-                  tc_ld16(tcol + 16 * c16, dd);
+                  for (int c16 = 0; c16 < kL; ++c16) tc_ld16_nowait(tcol + 16 * c16, dall[c16]);
+                  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                  tc_fence_before();
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive(&dempty[w * 2 + dbuf]);
 #pragma unroll
-                  for (int j = 0; j < 16; ++j) {
-                    const int col = 16 * c16 + j, b = col / kDigits, i = col % kDigits;
-                    if (b < MAXB) dacc[b] += (double)(int)dd[j] * kPow256[i];
+                  for (int c16 = 0; c16 < kL; ++c16)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                      const int col = 16 * c16 + j, b = col / kDigits, i = col % kDigits;
+                      if (b < MAXB) dacc[b] += (double)(int)dall[c16][j] * kPow256[i];
+                    }
+                } else {
+#pragma unroll
+                  for (int c16 = 0; c16 < kL; ++c16) {
+                    uint32_t dd[16];
+                    tc_ld16(tcol + 16 * c16, dd);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                      const int col = 16 * c16 + j, b = col / kDigits, i = col % kDigits;
+                      if (b < MAXB) dacc[b] += (double)(int)dd[j] * kPow256[i];
+                    }
                   }
+                  tc_fence_before();
+                  __syncwarp();
+                  if (lane == 0) mbar_arrive(&dempty[w * 2 + dbuf]);
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&dempty[w * 2 + dbuf]);
                 ++dcnt[w];
               }
             }
