@@ -328,10 +328,11 @@ __device__ __forceinline__ void decode_row(const uint32_t* w, uint32_t* o, const
 // row n = 8 nb + r (= 6 b + i; rows >= 6 B are zero), column k = 16 kc + kk of the
 // super-step.  sums: [nss][Bp] = sum over the super-step's columns of x * 2^24.
 __device__ __forceinline__ long long x_fixed(__half h) { return (long long)(__half2float(h) * 16777216.0f); }
-// The pass also zeroes the GEMV's synchronisation words (stream-K counters and
-// partial rows, `nzero` 16-byte words at `zero`): the GEMV's fixup treats a zero
-// partial word as "not written yet", and a workspace shared by calls of other
-// shapes holds their tiles / sums there.  CTAs past nss only zero.
+// The pass also zeroes the GEMV's stream-K counters when the GEMV grid is larger
+// than the SM count (`nzero` 16-byte words at `zero`; a workspace shared by calls
+// of other shapes may hold their data there).  CTAs past nss only zero.  (One
+// CTA per super-step: a grid of two CTAs per SM looping over super-steps, to fit
+// next to the running GEMV in one wave, measured slower.)
 __global__ void owq_x_digits_kernel(const __half* __restrict__ x, int64_t xK, int B, int Bp, int K, int NN,
                                     uint8_t* __restrict__ tiles, long long* __restrict__ sums, int nss,
                                     uint4* __restrict__ zero, int64_t nzero) {
