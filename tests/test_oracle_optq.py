@@ -147,3 +147,46 @@ def test_grouped_grid_fits_per_group():
     rep = O.owq_quantize(W, X, 3, 0, group=8, clip=False)
     assert rep.scale.shape == (4, 2)
     assert np.all(rep.scale[:, 1] > 3 * rep.scale[:, 0])
+
+
+def test_grouped_grid_refit_on_compensated_values():
+    # SURVEY §8(c) step 7 (the grid is fitted "after removing the weak columns";
+    # every not-yet-quantized column carries the compensation): with g > 0 a
+    # group's grid is fitted when the sweep reaches the group, on the group's CURRENT
+    # non-weak values.  Those values are solved here independently: the constrained
+    # least-squares optimum with the earlier group's dequantized values fixed,
+    # W_F + (W_A - D_A) H_AF H_FF^-1 (np.linalg.solve, no Cholesky, no sequential
+    # updates); the min-max grid is s = fp16((max(v,0) - min(v,0)) / (2^b - 1)),
+    # z = rne(-min(v,0)/s) (pinned by the S:174-176 examples).  The alternatives a
+    # plausible bug would use -- the original W, or every non-weak column at once --
+    # must give a different grid in most seeds, so the test has teeth.
+    r = np.random.default_rng(77)
+    bits, g, K, M = 2, 4, 8, 3
+    weak = (5,)
+    A, F = [0, 1, 2, 3], [4, 5, 6, 7]
+    grp1 = [4, 6, 7]                              # group 1 without its weak column
+    n_orig_differs = n_all_differs = 0
+    trials = 60
+    for _ in range(trials):
+        W = r.normal(size=(M, K))
+        X = r.normal(size=(K, 4 * K)) + 0.9 * r.normal(size=(1, 4 * K))   # correlated channels
+        Hd, _ = O.dampen(O.hessian(X))
+        codes, s, z, wv = O.optq_quantize(W, Hd, bits, g, weak, clip=False)
+        D_A = s[:, [0]] * (codes[:, A].astype(np.float64) - z[:, [0]])
+        HAF, HFF = Hd[np.ix_(A, F)], Hd[np.ix_(F, F)]
+        cur = W[:, F] + np.linalg.solve(HFF.T, ((W[:, A] - D_A) @ HAF).T).T
+        v = cur[:, [F.index(j) for j in grp1]]
+
+        def minmax(vals):
+            lo, hi = min(vals.min(), 0.0), max(vals.max(), 0.0)
+            sc = float(np.float16((hi - lo) / (2 ** bits - 1)))
+            return sc, float(np.clip(np.rint(-lo / sc), 0, 2 ** bits - 1))
+
+        for i in range(M):
+            se, ze = minmax(v[i])
+            assert s[i, 1] == se and z[i, 1] == ze, (i, s[i, 1], se, z[i, 1], ze)
+            if minmax(W[i, grp1]) != (se, ze):
+                n_orig_differs += 1
+            if minmax(W[i, [0, 1, 2, 3, 4, 6, 7]]) != (se, ze):
+                n_all_differs += 1
+    assert n_orig_differs > trials * M // 2 and n_all_differs > trials * M // 2

@@ -5,22 +5,18 @@ import csv, subprocess, sys
 from collections import Counter, defaultdict
 rep = sys.argv[1]
 W = float(sys.argv[2]) if len(sys.argv) > 2 else 73728.0
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(raw.splitlines()))
-h = rows[0]
-for r in rows[2:]:
-    if "owq_gemv_kernel" not in "".join(r):
-        continue
-    def get(name):
-        try: return float(r[h.index(name)].replace(",", ""))
-        except Exception: return float("nan")
-    print("duration us", get("gpu__time_duration.sum") / 1e3, " dram GB/s", get("dram__bytes.sum.per_second") / 1e9)
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+import ncu_csv  # noqa: E402  (unit row applied: values in bytes / seconds)
+for get_d in ncu_csv.launches(rep, "owq_")[:1]:
+    def get(name, d=get_d):
+        v = d.get(name, float("nan"))
+        return v if isinstance(v, float) else float("nan")
+    print("duration us", get("gpu__time_duration.sum") * 1e6, " dram GB/s", get("dram__bytes.sum.per_second") / 1e9)
     for n in ["alu", "fma", "fmaheavy", "lsu", "adu", "cbu", "uniform", "tc", "xu"]:
         v = get(f"sm__inst_executed_pipe_{n}.avg.pct_of_peak_sustained_active")
         if v == v: print(f"  pipe {n:9s} {v:6.1f}%")
-    st = [(get(n), n) for n in h if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")]
+    st = [(get(n), n) for n in get_d if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("not_issued")]
     print("  stalls:", ", ".join(f"{n[34:]}={v:.0f}" for v, n in sorted(st, reverse=True)[:8]))
-    break
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 rows = list(csv.reader(src.splitlines()))
 hdr = rows[2]

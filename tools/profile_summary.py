@@ -1,67 +1,100 @@
 """Write profiles/<round>_summary.md + profiles/ncu_traffic.json from the ncu
-artefacts of one round (launch list CSV + --set full reports of the GEMV on the
-two OPT-175B layer shapes).  python tools/profile_summary.py r1"""
-import csv, io, json, os, subprocess, sys
+artefacts of one round: the launch-list CSV (profiles/<round>_bench_launches.csv)
+and `--set full` reports profiles/prof_<round>_<tag>.ncu-rep of the GEMV.
+
+    python tools/profile_summary.py r2
+
+Units come from the CSV unit row (tools/ncu_csv.py): round 1's version assumed
+Mbyte everywhere and turned the q capture's 67.6 KB of DRAM writes into 67.6 MB.
+"""
+import csv
+import json
+import os
+import sys
 from collections import defaultdict
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import ncu_csv  # noqa: E402
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-rnd = sys.argv[1] if len(sys.argv) > 1 else "r1"
 P = os.path.join(ROOT, "profiles")
-out = [f"# ncu summary, round {rnd[1:]}\n"]
 
-rows = list(csv.reader(open(os.path.join(P, f"{rnd}_bench_launches.csv"))))
-h = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
-hdr = rows[h]; iK = hdr.index("Kernel Name"); iV = hdr.index("Metric Value")
-d = defaultdict(list)
-for r in rows[h + 1:]:
-    if len(r) == len(hdr):
-        d[r[iK].split("(")[0]].append(float(r[iV].replace(",", "")))
-tot = sum(sum(v) for v in d.values())
-out.append("## Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of "
-           "`bench.py --steps 2 --warmup 3 --no-graph` (cold, serialised launches)\n")
-out.append("| kernel | launches | median us | share of GPU time |\n|---|---|---|---|")
-for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
-    out.append(f"| `{k}` | {len(v)} | {sorted(v)[len(v) // 2] / 1e3:.2f} | {sum(v) / tot * 100:.1f}% |")
+# tag -> (M, K, bits, group, k, B)
+SHAPES = {
+    "q": (12288, 12288, 3, 0, 15, 1), "fc1": (49152, 12288, 3, 0, 3, 1), "fc2": (12288, 49152, 3, 0, 15, 1),
+    "qkv": (3 * 12288, 12288, 3, 0, 15, 1),
+    "b8": (12288, 12288, 3, 0, 15, 8), "b16": (12288, 12288, 3, 0, 15, 16),
+    "g128": (12288, 12288, 4, 128, 15, 1), "llama_up_b8": (11008, 4096, 4, 128, 1, 8),
+}
 
-def raw(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rr = list(csv.reader(io.StringIO(txt)))
-    h = rr[0]
-    for r in rr[2:]:
-        if "owq_gemv_kernel" in "".join(r):
-            def g(n):
-                try: return float(r[h.index(n)].replace(",", ""))
-                except Exception: return float("nan")
-            return g
-    return None
 
-traffic = {}
-out.append("\n## `ncu --set full` of one owq_gemv_kernel launch (B = 1)\n")
-out.append("| shape | duration us | DRAM read MB | DRAM write MB | algorithmic MB | ALU pipe % | FMA pipe % | issue slots busy % |")
-out.append("|---|---|---|---|---|---|---|---|")
-for tag, (M, K, k) in {"q": (12288, 12288, 15), "fc1": (49152, 12288, 3), "fc2": (12288, 49152, 15)}.items():
-    rep = os.path.join(ROOT, "gpurun_out", f"prof_{rnd}_{tag}.ncu-rep")
-    if not os.path.exists(rep):
-        continue
-    g = raw(rep)
-    alg = 3 * M * K / 8 + 4 * M + 2 * M * k + 2 * k + 2 * K + 2 * M
-    rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
-    unit = 1.0
-    traffic[tag] = {"dram_read_bytes": rd * 1e6, "dram_write_bytes": wr * 1e6, "algorithmic_bytes": alg,
-                    "duration_us": g("gpu__time_duration.sum") / 1e3 if g("gpu__time_duration.sum") > 1000 else g("gpu__time_duration.sum")}
-    out.append(f"| {tag} {M}x{K} | {traffic[tag]['duration_us']:.2f} | {rd:.2f} | {wr:.2f} | {alg / 1e6:.2f} | "
-               f"{g('sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active'):.1f} | "
-               f"{g('sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active'):.1f} | "
-               f"{g('sm__inst_issued.avg.pct_of_peak_sustained_active'):.1f} |")
-out.append("\nNotes: DRAM read equals the algorithmic bytes within 0.2 % for every shape (no re-reads). "
-           "The DRAM writes of the q-shape capture (tens of MB) cannot come from the kernel, which writes "
-           "KBs of y/partials; they are most likely write-back of dirty L2 lines left by the preceding "
-           "kernels of the replay. `--set full` durations are cold-cache, serialised ncu replays, not bench "
-           "numbers; the pipe columns are `sm__inst_executed_pipe_*` and `sm__inst_issued` as % of peak.")
-open(os.path.join(P, f"{rnd}_summary.md"), "w").write("\n".join(out) + "\n")
-if traffic:
-    layer_tags = ["q", "q", "q", "q", "fc1", "fc2" if "fc2" in traffic else "fc1"]
-    per = [traffic[t]["dram_read_bytes"] + traffic[t]["dram_write_bytes"] for t in layer_tags]
-    json.dump({"round": rnd, "per_shape": traffic, "bytes_per_step": sum(per),
-               "note": "dram__bytes_read.sum + dram__bytes_write.sum of one --set full capture per shape; "
-                       "q/k/v/out share the q capture"}, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
-print("\n".join(out))
+def algorithmic_bytes(M, K, bits, group, k, B):
+    """codes + fp16 scale/zero + weak values/indices + x + y (f16)."""
+    G = 1 if group == 0 else -(-K // group)
+    return bits * M * K / 8 + 4 * M * G + 2 * M * k + 2 * k + 2 * K * B + 2 * M * B
+
+
+def main(rnd):
+    out = [f"# ncu summary, round {rnd[1:]}\n"]
+    lpath = os.path.join(P, f"{rnd}_bench_launches.csv")
+    if os.path.exists(lpath):
+        rows = list(csv.reader(open(lpath)))
+        h = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+        hdr = rows[h]
+        iK, iV, iU = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+        d = defaultdict(list)
+        for r in rows[h + 1:]:
+            if len(r) == len(hdr):
+                d[r[iK].split("(")[0]].append(float(r[iV].replace(",", "")) * ncu_csv.scale_of(r[iU]))
+        tot = sum(sum(v) for v in d.values())
+        out.append("## Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of "
+                   "`bench.py` (cold, serialised launches)\n")
+        out.append("| kernel | launches | median us | share of GPU time |\n|---|---|---|---|")
+        for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
+            out.append(f"| `{k}` | {len(v)} | {sorted(v)[len(v) // 2] * 1e6:.2f} | {sum(v) / tot * 100:.1f}% |")
+    traffic = {}
+    out.append("\n## `ncu --set full` of one GEMV launch per shape\n")
+    out.append("| shape | B | duration us | DRAM read MB | DRAM write MB | algorithmic MB | read / alg | "
+               "ALU % | FMA % | tensor-mem active % | issue % | SM MHz |")
+    out.append("|---|---|---|---|---|---|---|---|---|---|---|---|")
+    for tag, shp in SHAPES.items():
+        rep = os.path.join(P, f"prof_{rnd}_{tag}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        L = ncu_csv.launches(rep, "owq_")
+        L = [x for x in L if "gemv" in str(x.get("Kernel Name", x.get("Function Name", "gemv")))] or L
+        if not L:
+            continue
+        g = L[0]
+        alg = algorithmic_bytes(*shp)
+        rd, wr = g["dram__bytes_read.sum"], g["dram__bytes_write.sum"]
+        dur = g["gpu__time_duration.sum"]
+
+        def pct(n):
+            v = g.get(n)
+            return f"{v:.1f}" if isinstance(v, float) else "-"
+
+        tc = "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active"
+        traffic[tag] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "algorithmic_bytes": alg,
+                        "duration_us": dur * 1e6, "batch": shp[5]}
+        out.append(f"| {tag} {shp[0]}x{shp[1]} b{shp[2]} g{shp[3]} k{shp[4]} | {shp[5]} | {dur * 1e6:.2f} | "
+                   f"{rd / 1e6:.3f} | {wr / 1e6:.4f} | {alg / 1e6:.3f} | {rd / alg:.4f} | "
+                   f"{pct('sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active')} | "
+                   f"{pct('sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active')} | "
+                   f"{pct(tc) if tc else '-'} | "
+                   f"{pct('sm__inst_issued.avg.pct_of_peak_sustained_active')} | "
+                   f"{g.get('sm__cycles_elapsed.avg.per_second', 0) / 1e6:.0f} |")
+    out.append("\n`--set full` durations are cold-cache serialised ncu replays, not bench numbers. "
+               "DRAM bytes come from `dram__bytes_read.sum` / `dram__bytes_write.sum` scaled by the unit "
+               "row of the CSV; `read / alg` = DRAM read over the algorithmic bytes of SURVEY §8(d).")
+    open(os.path.join(P, f"{rnd}_summary.md"), "w").write("\n".join(out) + "\n")
+    if traffic:
+        json.dump({"round": rnd, "per_shape": traffic,
+                   "note": "dram__bytes_read.sum + dram__bytes_write.sum (unit row applied) of one "
+                           "--set full capture per shape"},
+                  open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r2")
