@@ -58,7 +58,8 @@
 extern "C" {
 #endif
 
-#define OWQ_LAYOUT_VERSION 3
+#define OWQ_LAYOUT_VERSION 3   /* tensor-core layout (tcgen05 kind::i8 GEMV)          */
+#define OWQ_LAYOUT_CC 4        /* CUDA-core layout (FFMA2 GEMV), see owq_pack flags   */
 #define OWQ_MAX_BATCH 16
 
 typedef enum {
@@ -100,10 +101,21 @@ typedef struct {
 /* owq_pack flags */
 #define OWQ_PACK_STRICT 1    /* reject weak-column codes != z instead of zero-filling */
 #define OWQ_PACK_U8_CODES 2  /* layer->codes is one code per byte, [c_out][c_in]       */
+#define OWQ_PACK_LAYOUT_CC 4 /* write device layout 4 (CUDA-core GEMV) instead of 3      */
 
 /* Bytes of the device blob for `shape` (header + padded code units + weak
- * units + scale/zero blocks + weak index list).  0 on an invalid shape. */
+ * units + scale/zero blocks + weak index list) in layout 3.  0 on an invalid
+ * shape. */
 size_t owq_packed_bytes(const owq_shape *shape);
+
+/* Bytes of the device blob for `shape` in `layout` (OWQ_LAYOUT_VERSION = 3,
+ * the tensor-core layout, or OWQ_LAYOUT_CC = 4, the CUDA-core layout: items of
+ * 128 rows x 32 columns in which every code is one LOP3 away from an fp32
+ * subnormal).  0 on an invalid shape or layout.  Both layouts
+ * hold the same representation in the same number of code bytes
+ * (b*M*K/8 up to row/column padding); the GEMV entry points read the layout
+ * from the blob header and run the matching kernel. */
+size_t owq_packed_bytes_layout(const owq_shape *shape, int layout);
 
 /* Host packer (C++, runs once per layer, off the hot path): validates the
  * paper representation and writes the device layout into h_blob.  Weak-column
@@ -113,7 +125,9 @@ owq_status owq_pack_host(const owq_shape *shape, const owq_host_layer *layer,
                          int flags, void *h_blob, size_t blob_bytes);
 
 /* owq_pack_host into a temporary host buffer, then a copy to d_packed on
- * `stream`; returns after the copy completed (packing is offline). */
+ * `stream`; returns after the copy completed (packing is offline).  With
+ * OWQ_PACK_LAYOUT_CC in flags the blob is layout 4 and d_bytes must be at
+ * least owq_packed_bytes_layout(shape, OWQ_LAYOUT_CC). */
 owq_status owq_pack(const owq_shape *shape, const owq_host_layer *layer,
                     int flags, void *d_packed, size_t d_bytes, void *stream);
 
@@ -139,6 +153,11 @@ owq_status owq_unpack_codes(const owq_shape *shape, const void *d_packed,
  * for the largest shape) serves sequential calls of any shapes.  One workspace
  * must not be used by two calls that may run concurrently. */
 size_t owq_workspace_bytes(const owq_shape *shape, int batch);
+
+/* Workspace for an explicit grid (owq_gemm_small_batch_grid; 0 = the default
+ * grid of the current device), for either layout.  0 on an invalid shape,
+ * batch or grid. */
+size_t owq_workspace_bytes_grid(const owq_shape *shape, int batch, int grid);
 
 /* y = W_hat x for one activation vector (batch 1).
  * d_x: fp16 [c_in] (finite values); d_y: [c_out], fp32 if y_f32 else fp16 (RNE).

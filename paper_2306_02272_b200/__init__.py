@@ -25,19 +25,21 @@ __all__ = [
     "owq_tp_get_unique_id", "owq_tp_init", "owq_tp_destroy", "owq_tp_bounds",
     "owq_tp_shard_shape", "owq_tp_shard_host", "owq_tp_shard", "owq_tp_workspace_bytes",
     "owq_tp_gemv", "OwqLinear", "OWQ_TP_ROWS", "OWQ_TP_COLS", "OWQ_PACK_STRICT",
-    "OWQ_PACK_U8_CODES", "EXPORTED_SYMBOLS",
+    "OWQ_PACK_U8_CODES", "OWQ_PACK_LAYOUT_CC", "OWQ_LAYOUT_TC", "OWQ_LAYOUT_CC",
+    "owq_packed_bytes_layout", "owq_workspace_bytes_grid", "EXPORTED_SYMBOLS",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("OWQ_LIB") or os.path.join(HERE, "libowq.so")   # OWQ_LIB: A/B experiments only
 
 OWQ_TP_ROWS, OWQ_TP_COLS = 0, 1
-OWQ_PACK_STRICT, OWQ_PACK_U8_CODES = 1, 2
+OWQ_PACK_STRICT, OWQ_PACK_U8_CODES, OWQ_PACK_LAYOUT_CC = 1, 2, 4
+OWQ_LAYOUT_TC, OWQ_LAYOUT_CC = 3, 4     # device layouts: tensor-core (tcgen05) / CUDA-core
 
 # every symbol include/owq.h declares
 EXPORTED_SYMBOLS = [
-    "owq_packed_bytes", "owq_pack_host", "owq_pack", "owq_blob_decode_host",
-    "owq_unpack_codes", "owq_workspace_bytes", "owq_gemv", "owq_gemm_small_batch",
+    "owq_packed_bytes", "owq_packed_bytes_layout", "owq_pack_host", "owq_pack", "owq_blob_decode_host",
+    "owq_unpack_codes", "owq_workspace_bytes", "owq_workspace_bytes_grid", "owq_gemv", "owq_gemm_small_batch",
     "owq_gemm_small_batch_grid", "owq_tp_get_unique_id", "owq_tp_init", "owq_tp_destroy",
     "owq_tp_shard_shape", "owq_tp_shard_host", "owq_tp_shard", "owq_tp_workspace_bytes",
     "owq_tp_gemv", "owq_tp_bounds", "owq_status_string",
@@ -83,6 +85,8 @@ def lib():
     sz = ctypes.c_size_t
     sig = {
         "owq_packed_bytes": (sz, [_S]),
+        "owq_packed_bytes_layout": (sz, [_S, ctypes.c_int]),
+        "owq_workspace_bytes_grid": (sz, [_S, ctypes.c_int, ctypes.c_int]),
         "owq_pack_host": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.c_int, _P, sz]),
         "owq_pack": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.c_int, _P, sz, _P]),
         "owq_blob_decode_host": (st, [_P, sz, _S, _P, _P, _P, _P, _P]),
@@ -190,9 +194,17 @@ def owq_packed_bytes(shape) -> int:
     return int(lib().owq_packed_bytes(ctypes.byref(_shape(shape))))
 
 
+def owq_packed_bytes_layout(shape, layout: int) -> int:
+    return int(lib().owq_packed_bytes_layout(ctypes.byref(_shape(shape)), int(layout)))
+
+
+def _layout_of(flags: int) -> int:
+    return OWQ_LAYOUT_CC if flags & OWQ_PACK_LAYOUT_CC else OWQ_LAYOUT_TC
+
+
 def owq_pack_host(shape, rep: dict, flags: int = 0) -> np.ndarray:
     s = _shape(shape)
-    n = owq_packed_bytes(s)
+    n = owq_packed_bytes_layout(s, _layout_of(flags))
     if n == 0:
         raise OwqError("OWQ_ERR_UNSUPPORTED")
     blob = np.empty(n, dtype=np.uint8)
@@ -204,13 +216,14 @@ def owq_pack_host(shape, rep: dict, flags: int = 0) -> np.ndarray:
 def owq_pack(shape, rep: dict, flags: int = 0, device=None, stream=None):
     import torch
     s = _shape(shape)
-    n = owq_packed_bytes(s)
+    n = owq_packed_bytes_layout(s, _layout_of(flags))
     if n == 0:
         raise OwqError("OWQ_ERR_UNSUPPORTED")
     d = torch.empty(n, dtype=torch.uint8, device=device or "cuda")
     hl, flags = _layer_from(rep, flags)
-    _check(lib().owq_pack(ctypes.byref(s), ctypes.byref(hl.layer), flags, d.data_ptr(), n,
-                          _stream(stream)))
+    with torch.cuda.device(d.device):
+        _check(lib().owq_pack(ctypes.byref(s), ctypes.byref(hl.layer), flags, d.data_ptr(), n,
+                              _stream(stream)))
     return d
 
 
@@ -241,14 +254,21 @@ def owq_workspace_bytes(shape, batch: int = 1) -> int:
     return int(lib().owq_workspace_bytes(ctypes.byref(_shape(shape)), batch))
 
 
+def owq_workspace_bytes_grid(shape, batch: int = 1, grid: int = 0) -> int:
+    return int(lib().owq_workspace_bytes_grid(ctypes.byref(_shape(shape)), batch, grid))
+
+
 def workspace(shape, batch: int = 1, device=None, grid: int = 0):
     """Zero-filled workspace (every call leaves its stream-K slots and counters
-    at zero again, so one workspace serves sequential calls of any shapes)."""
+    at zero again, so one workspace serves sequential calls of any shapes).
+    The size comes from the C ABI (owq_workspace_bytes_grid) on `device`."""
     import torch
-    n = owq_workspace_bytes(shape, batch)
-    if grid:   # stream-K partial slots for a non-default grid: grid x batch x 128 rows x f32
-        n = n + grid * batch * 128 * 4
-    return torch.zeros(max(n, 256), dtype=torch.uint8, device=device or "cuda")
+    dev = torch.device(device or "cuda")
+    with torch.cuda.device(dev):
+        n = owq_workspace_bytes_grid(shape, batch, grid)
+    if n == 0:
+        raise OwqError("OWQ_ERR_UNSUPPORTED (workspace for this shape / batch / grid)")
+    return torch.zeros(max(n, 256), dtype=torch.uint8, device=dev)
 
 
 def _out(s: Shape, B: int, y, y_f32: bool, device):
@@ -258,13 +278,51 @@ def _out(s: Shape, B: int, y, y_f32: bool, device):
     return y
 
 
+def _check_io(s: Shape, d_packed, x, y, y_f32: bool, B: int, ws):
+    """Every tensor the C ABI will dereference: dtype, contiguity, shape and
+    device (the ABI takes raw pointers, so a wrong tensor would otherwise be
+    read or written out of bounds)."""
+    import torch
+    dev = d_packed.device
+    if d_packed.dtype != torch.uint8 or not d_packed.is_contiguous():
+        raise OwqError("packed blob must be a contiguous uint8 tensor")
+    if x.dtype != torch.float16:
+        raise OwqError(f"x must be float16, got {x.dtype}")
+    if x.device != dev:
+        raise OwqError(f"x is on {x.device}, the layer on {dev}")
+    if not x.is_contiguous():
+        raise OwqError("x must be contiguous (row-major [B][c_in])")
+    if tuple(x.shape) not in ((B, s.c_in),) and not (x.dim() == 1 and B == 1 and x.shape[0] == s.c_in):
+        raise OwqError(f"x must be [{B}][{s.c_in}], got {tuple(x.shape)}")
+    want = torch.float32 if y_f32 else torch.float16
+    if y.dtype != want:
+        raise OwqError(f"y must be {want} (y_f32={bool(y_f32)}), got {y.dtype}")
+    if y.device != dev or not y.is_contiguous():
+        raise OwqError("y must be contiguous and on the layer's device")
+    if y.numel() != B * s.c_out:
+        raise OwqError(f"y must hold [{B}][{s.c_out}] elements, got {tuple(y.shape)}")
+    if ws is not None and (ws.device != dev or ws.dtype != torch.uint8 or not ws.is_contiguous()):
+        raise OwqError("workspace must be a contiguous uint8 tensor on the layer's device")
+
+
+def _on_device(dev):
+    """torch.cuda.device(dev) unless dev is already current (saves ~2 us per call)."""
+    import contextlib
+    import torch
+    if dev.index is None or dev.index == torch._C._cuda_getDevice():
+        return contextlib.nullcontext()
+    return torch.cuda.device(dev)
+
+
 def owq_gemv(shape, d_packed, x, y=None, y_f32=False, ws=None, stream=None):
     """y = W_hat x for one fp16 vector x [c_in] (or [1][c_in]); returns y [1][c_out]."""
     s = _shape(shape)
     y = _out(s, 1, y, y_f32, x.device)
-    ws = ws if ws is not None else workspace(s, 1, x.device)
-    _check(lib().owq_gemv(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), y.data_ptr(),
-                          int(bool(y_f32)), ws.data_ptr(), ws.numel(), _stream(stream)))
+    _check_io(s, d_packed, x, y, y_f32, 1, ws)
+    with _on_device(d_packed.device):
+        ws = ws if ws is not None else workspace(s, 1, x.device)
+        _check(lib().owq_gemv(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), y.data_ptr(),
+                              int(bool(y_f32)), ws.data_ptr(), ws.numel(), _stream(stream)))
     return y
 
 
@@ -273,10 +331,12 @@ def owq_gemm_small_batch(shape, d_packed, x, y=None, y_f32=False, ws=None, strea
     s = _shape(shape)
     B = x.shape[0] if x.dim() == 2 else 1
     y = _out(s, B, y, y_f32, x.device)
-    ws = ws if ws is not None else workspace(s, B, x.device)
-    _check(lib().owq_gemm_small_batch(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B,
-                                      y.data_ptr(), int(bool(y_f32)), ws.data_ptr(), ws.numel(),
-                                      _stream(stream)))
+    _check_io(s, d_packed, x, y, y_f32, B, ws)
+    with _on_device(d_packed.device):
+        ws = ws if ws is not None else workspace(s, B, x.device)
+        _check(lib().owq_gemm_small_batch(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B,
+                                          y.data_ptr(), int(bool(y_f32)), ws.data_ptr(), ws.numel(),
+                                          _stream(stream)))
     return y
 
 
@@ -284,10 +344,12 @@ def owq_gemm_small_batch_grid(shape, d_packed, x, grid: int, y=None, y_f32=False
     s = _shape(shape)
     B = x.shape[0] if x.dim() == 2 else 1
     y = _out(s, B, y, y_f32, x.device)
-    ws = ws if ws is not None else workspace(s, B, x.device, grid=grid)
-    _check(lib().owq_gemm_small_batch_grid(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B,
-                                           y.data_ptr(), int(bool(y_f32)), ws.data_ptr(), ws.numel(),
-                                           grid, _stream(stream)))
+    _check_io(s, d_packed, x, y, y_f32, B, ws)
+    with _on_device(d_packed.device):
+        ws = ws if ws is not None else workspace(s, B, x.device, grid=grid)
+        _check(lib().owq_gemm_small_batch_grid(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B,
+                                               y.data_ptr(), int(bool(y_f32)), ws.data_ptr(), ws.numel(),
+                                               grid, _stream(stream)))
     return y
 
 
@@ -365,10 +427,19 @@ def owq_tp_gemv(tp, mode, full, shard, d_packed, x, y, y_f32=False, ws=None, str
 class OwqLinear:
     """A packed OWQ layer resident in HBM: ``y = layer(x)`` (x fp16 [B][c_in])."""
 
-    def __init__(self, rep: dict, device=None, max_batch: int = 16, flags: int = 0):
+    def __init__(self, rep: dict, device=None, max_batch: int = 16, flags: int = 0, layout: int = None):
+        """layout: OWQ_LAYOUT_TC (tcgen05 kernel) or OWQ_LAYOUT_CC (CUDA-core kernel);
+        None = OWQ_LAYOUT_CC when max_batch <= 4 (decode), else OWQ_LAYOUT_TC."""
         import torch
         self.shape = _shape((rep["M"], rep["K"], rep["bits"], rep["group"], len(rep["weak_idx"])))
         self.device = torch.device(device or "cuda")
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        if layout is None:
+            layout = OWQ_LAYOUT_CC if max_batch <= 4 else OWQ_LAYOUT_TC
+        if layout == OWQ_LAYOUT_CC:
+            flags |= OWQ_PACK_LAYOUT_CC
+        self.layout = layout
         self.packed = owq_pack(self.shape, rep, flags, device=self.device)
         self.ws = workspace(self.shape, max_batch, self.device)
 

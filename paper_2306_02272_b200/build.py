@@ -17,9 +17,9 @@ BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU = ["owq_gemv.cu", "owq_tp.cu"]
+CU = ["owq_gemv.cu", "owq_gemv_cc.cu", "owq_tp.cu"]
 CPP = ["owq_pack.cpp"]
-HDRS = ["owq_layout.h"]
+HDRS = ["owq_layout.h", "owq_layout_cc.h"]
 
 
 def nccl_dirs():
@@ -47,10 +47,12 @@ def needs_build(force=False):
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def build(force: bool = False, verbose: bool = False, csrc: str = None, out: str = None, inc: str = None) -> str:
-    """csrc/out/inc: experiments only (A/B builds of another source tree into another file)."""
+def build(force: bool = False, verbose: bool = False, csrc: str = None, out: str = None, inc: str = None,
+          defines=()) -> str:
+    """csrc/out/inc/defines: experiments only (A/B builds of another source tree or
+    with -D knobs into another file; the product build uses the defaults)."""
     global CSRC, OUT, BUILD, INC
-    if csrc or out or inc:
+    if csrc or out or inc or defines:
         CSRC, OUT, INC = csrc or CSRC, out or OUT, inc or INC
         BUILD = OUT + "_build"
         force = True
@@ -61,7 +63,7 @@ def build(force: bool = False, verbose: bool = False, csrc: str = None, out: str
     objs = []
     for f in CU:
         o = os.path.join(BUILD, f + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        cmd = [NVCC, *ARCH, *[f"-D{d}" for d in defines], "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3",
                "-I", INC, "-I", CSRC, "-I", ninc, "-c", os.path.join(CSRC, f), "-o", o]
         r = _run(cmd)
@@ -83,4 +85,5 @@ def build(force: bool = False, verbose: bool = False, csrc: str = None, out: str
 if __name__ == "__main__":
     a = sys.argv
     opt = lambda k: a[a.index(k) + 1] if k in a else None
-    print(build(force="--force" in a, verbose="-v" in a, csrc=opt("--csrc"), out=opt("--out"), inc=opt("--inc")))
+    print(build(force="--force" in a, verbose="-v" in a, csrc=opt("--csrc"), out=opt("--out"), inc=opt("--inc"),
+                defines=[a[i + 1] for i, v in enumerate(a) if v == "-D"]))

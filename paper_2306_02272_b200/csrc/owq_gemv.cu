@@ -38,18 +38,47 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "owq.h"
 #include "owq_layout.h"
+#include "owq_layout_cc.h"
 
 namespace owq {
+namespace cc {   // owq_gemv_cc.cu
+owq_status gemm(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, void* ws, size_t ws_bytes,
+                int grid_req, cudaStream_t stream);
+owq_status unpack(const Geo& g, const void* blob, uint8_t* codes, cudaStream_t stream);
+int grid_for(const Geo& g, int grid_req);
+size_t workspace_bytes(int grid, int nb);
+}  // namespace cc
+}  // namespace owq
+
+namespace owq {
+
+// Experiment hooks (environment knobs, per-CTA timestamp traces) exist only in
+// builds with -DOWQ_EXPERIMENTS (tools/ab_build.sh); the product library ignores
+// the environment and carries no trace code.
+#ifdef OWQ_EXPERIMENTS
+constexpr bool kTrace = true;
+static int knob(const char* name, int def) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : def;
+}
+#define OWQ_CLK() clock64()
+#else
+constexpr bool kTrace = false;
+static inline int knob(const char*, int def) { return def; }
+#define OWQ_CLK() 0ll
+#endif
 
 constexpr int kDigits = 6;          // int8 digits per x value (base 256, balanced)
 
 // MMA N (digit rows of B) for a batch: 6 * B padded to a valid tcgen05 N
 static inline int mma_n_for(int B) {
-  static const int min_n = getenv("OWQ_MINN") ? atoi(getenv("OWQ_MINN")) : 8;   // experiments
+  static const int min_n = knob("OWQ_MINN", 8);
   const int r = std::max(kDigits * B, min_n);
   return r <= 8 ? 8 : r <= 16 ? 16 : r <= 32 ? 32 : r <= 64 ? 64 : 96;
 }
@@ -74,7 +103,7 @@ struct Params {
   int32_t code_bytes;     // stage region for codes / weak chunks
   int32_t tile_off;       // digit tiles inside a stage
   int32_t sum_off;        // per-item digit sums inside a stage (in-kernel digit mode)
-  int32_t x_off;          // raw x columns of the stage, B rows of cap*64 fp16 (in-kernel digit mode)
+  int32_t x_off;          // end of the staged digit sums (grouped per-stage mode)
   int32_t sz_off;         // scale/zero blocks of the stage's groups (grouped per-stage mode)
   int32_t gstage;         // grouped per-stage mode: the epilogue consumes the ring (sums + s/z staged)
   int32_t stage_bytes;
@@ -371,41 +400,6 @@ __global__ void owq_x_digits_kernel(const __half* __restrict__ x, int64_t xK, in
   if (k == 0) sums[(int64_t)ss * Bp + b] = part[2 * b] + part[2 * b + 1];
 }
 
-// Balanced base-256 digits of X (|X| < 2^40) as the bytes of
-// (X + 0x808080808080) ^ 0x808080808080: byte i = b_i - 128 in two's complement
-// where b_i are the bytes of X + sum 128*256^i (carries included), so
-// sum_i (int8)byte_i 256^i = X.
-__device__ __forceinline__ unsigned long long digit_bytes(long long X) {
-  return (unsigned long long)(X + 0x808080808080LL) ^ 0x808080808080ULL;
-}
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-  return d;
-}
-// w[i] = digit i of the 4 values (byte j = value j), i < 6
-__device__ __forceinline__ void digits4(const unsigned long long* v, uint32_t* w) {
-  const uint32_t l0 = (uint32_t)v[0], l1 = (uint32_t)v[1], l2 = (uint32_t)v[2], l3 = (uint32_t)v[3];
-  const uint32_t h0 = (uint32_t)(v[0] >> 32), h1 = (uint32_t)(v[1] >> 32), h2 = (uint32_t)(v[2] >> 32),
-                 h3 = (uint32_t)(v[3] >> 32);
-  const uint32_t a01 = prmt(l0, l1, 0x5140), a23 = prmt(l2, l3, 0x5140);   // bytes 0,1 interleaved
-  const uint32_t b01 = prmt(l0, l1, 0x7362), b23 = prmt(l2, l3, 0x7362);   // bytes 2,3 interleaved
-  const uint32_t c01 = prmt(h0, h1, 0x5140), c23 = prmt(h2, h3, 0x5140);   // bytes 4,5 interleaved
-  w[0] = prmt(a01, a23, 0x5410); w[1] = prmt(a01, a23, 0x7632);
-  w[2] = prmt(b01, b23, 0x5410); w[3] = prmt(b01, b23, 0x7632);
-  w[4] = prmt(c01, c23, 0x5410); w[5] = prmt(c01, c23, 0x7632);
-}
-
-// x rows whose stride or base breaks 16-byte TMA alignment are first copied
-// into a zero-padded [B][Kp] buffer in the workspace (Kp = K rounded up to 64).
-__global__ void owq_pad_x_kernel(const __half* __restrict__ x, __half* __restrict__ xp, int B, int K, int Kp) {
-  const int64_t n = (int64_t)B * Kp;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(i / Kp), c = (int)(i - (int64_t)b * Kp);
-    xp[i] = c < K ? x[(int64_t)b * K + c] : __float2half(0.f);
-  }
-}
-
 // group of code item li (row-block relative super-step index)
 __device__ __forceinline__ int group_of(const Params& p, int li) { return p.g.group ? (li >> p.group_log2) : 0; }
 
@@ -420,10 +414,9 @@ struct Cfg {
   // Implemented, but measured slower at batch 1 (the decode becomes the limit and
   // the extra MMA concurrency adds TMEM contention): 1 everywhere.
   static constexpr int ISS = 1;
-  // In-kernel digit mode (decode warps turn the stage's raw x into digit tiles,
-  // no pre-pass) is implemented but off: measured slower on B200 (12288^2 B=1:
-  // 28.2 us vs 24.0 us) because it lengthens the decode warps' stage.
-  static constexpr bool kInDig = false;
+  // (In-kernel digit mode -- decode warps turning the stage's raw x into digit
+  // tiles instead of the pre-pass -- was measured slower on B200, 12288^2 B=1:
+  // 28.2 us vs 24.0 us, and removed.)
   static constexpr int kIPW0 = (512 - 2 * ISS * DWG * NN) / (2 * DWG * 16);
   // 7 items per warpgroup at batch 1 (measured -8 % vs 6); grouped-scale kernels
   // keep 6 so the per-stage D blocks (kGP) fit next to the A buffers
@@ -529,7 +522,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
 
   const int64_t grid = gridDim.x, cta = blockIdx.x;
   if (threadIdx.x == 0) {
-    if (p.trace) p.trace[cta * 256 + 0] = gtime();
+    if (kTrace && p.trace) p.trace[cta * 256 + 0] = gtime();
     span[0] = p.span[cta];
     span[1] = p.span[cta + 1];
     for (int s = 0; s < NST; ++s) {
@@ -551,7 +544,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int64_t i0 = span[0], i1 = span[1];
-  if (p.trace && threadIdx.x == 0) {
+  if (kTrace && p.trace && threadIdx.x == 0) {
     p.trace[cta * 256 + 58] = (unsigned long long)i0;
     p.trace[cta * 256 + 59] = (unsigned long long)i1;
     p.trace[cta * 256 + 61] = (unsigned long long)items_per_rb(g);
@@ -602,8 +595,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           if (!dep) resolve();
           mbar_wait(&empty[s], ph ^ 1u);
         }
-        if (p.trace && k < 32) p.trace[cta * 256 + 64 + k] = gtime();
-        const bool code = true;
+        if (kTrace && p.trace && k < 32) p.trace[cta * 256 + 64 + k] = gtime();
         uint32_t fl = 0;
         if (nn == 0 || nrb != srb) fl |= kRbEnd;
         else if (group_of(p, nli) == group_of(p, sli + n - 1)) fl |= kGroupCont;
@@ -611,7 +603,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
                      "r"((uint32_t)(sli & 0xFFFF) | ((uint32_t)n << 16) | (fl << 24)) : "memory");
         uint8_t* st = ring + (size_t)s * p.stage_bytes;
         const uint32_t cbytes = (uint32_t)stage_bytes(g, sli, n);
-        if (code && !C::kInDig) {
+        {
           // codes -> full[s] (decode), digit tiles -> tready[s] (MMA only), so the
           // decode can run while the x-digit pass is still producing the tiles
           const uint32_t sumb = p.gstage ? (uint32_t)(n * p.Bp * 8) : 0u;
@@ -632,17 +624,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           } else {
             pend_sli[npend] = sli; pend_n[npend] = n; pend_s[npend] = s; ++npend;
           }
-        } else if (code) {
-          // codes + the x columns of the stage (x rows are 16-byte aligned, K % 8 == 0: host-checked)
-          const int64_t col0 = (int64_t)sli * kSuperStep;
-          const int64_t xc = p.xK - col0 < (int64_t)n * kSuperStep ? p.xK - col0 : (int64_t)n * kSuperStep;
-          mbar_expect_tx(&full[s], cbytes + (uint32_t)(p.B * xc * 2));
-          bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
-          for (int b = 0; b < p.B; ++b)
-            bulk_g2s(st + p.x_off + b * p.cap * kSuperStep * 2, p.x + (int64_t)b * p.xK + col0, (uint32_t)(xc * 2), &full[s], pol_x);
-        } else {
-          mbar_expect_tx(&full[s], cbytes);
-          bulk_g2s(st, p.blob + g.units_off + item_offset(g, srb, sli), cbytes, &full[s], pol);
         }
         ++k;
         if (++s == NST) { s = 0; ph ^= 1u; }
@@ -712,7 +693,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
             decode_row<BITS>(w, o, sh);
             tc_st16(tcol + t * C::kACols, o);
           };
-          if (p.exp == 3) {
+          if (kTrace && p.exp == 3) {
           } else if (hi - lo == C::kIPW) {   // full share: unrolled, immediate offsets
 #pragma unroll
             for (int t = 0; t < C::kIPW; ++t) {
@@ -726,37 +707,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
               load_item(t, w);
               store_item(t, w);
             }
-          }
-          if (C::kInDig) {
-            // digit tiles of this warpgroup's items: warp q converts items lo+q, lo+q+4, ..
-            // lane = (batch row bb, columns 4*nl .. 4*nl+3)
-            const int nl = lane & 15, bb = lane >> 4;
-            for (int pi = lo + q; pi < hi; pi += 4) {
-              const int64_t col0 = (int64_t)(d.li + pi) * kSuperStep + nl * 4;
-              const uint32_t tb = sbase + (uint32_t)p.tile_off + (uint32_t)pi * (uint32_t)(NN * kSuperStep) +
-                                  (uint32_t)(nl >> 2) * (NN / 8) * 128 + (uint32_t)(nl & 3) * 4;
-              if (bb < p.B) {
-                const uint2 xr = lds64(sbase + (uint32_t)p.x_off + (uint32_t)(bb * p.cap * kSuperStep + pi * kSuperStep + nl * 4) * 2u);
-                const uint32_t xh[2] = {xr.x, xr.y};
-                unsigned long long v[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const __half h = __ushort_as_half((unsigned short)(xh[j >> 1] >> (16 * (j & 1))));
-                  v[j] = digit_bytes(col0 + j < g.K ? x_fixed(h) : 0);
-                }
-                uint32_t wd[kDigits];
-                digits4(v, wd);
-#pragma unroll
-                for (int i = 0; i < kDigits; ++i) {
-                  const int n = kDigits * bb + i;
-                  asm volatile("st.shared.u32 [%0], %1;" ::"r"(tb + (uint32_t)((n >> 3) * 128 + (n & 7) * 16)), "r"(wd[i]) : "memory");
-                }
-              }
-              if (bb == 0)
-                for (int n = kDigits * p.B; n < NN; ++n)
-                  asm volatile("st.shared.u32 [%0], %1;" ::"r"(tb + (uint32_t)((n >> 3) * 128 + (n & 7) * 16)), "r"(0u) : "memory");
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // tiles -> async proxy (MMA)
           }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
@@ -809,15 +759,15 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       const int32_t sli = dsc.li, n = dsc.n;
       const uint32_t buf = (uint32_t)j & 1u;
       if (ISS == 1 || (int)buf == ii) {
-        const long long t0 = clock64();
+        const long long t0 = OWQ_CLK();
         mbar_wait(&afull[wg * 2 + buf], ((uint32_t)j >> 1) & 1u);
-        const long long t1 = clock64();
+        const long long t1 = OWQ_CLK();
         c_wait += t1 - t0;
         int lo, hi;
         share<DWG>(n, wg, lo, hi);
-        if (!C::kInDig) mbar_wait(&tready[s], (uint32_t)(j / NST) & 1u);   // this stage's digit tiles
-        c_tready += clock64() - t1;
-        if (p.trace && dq == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
+        mbar_wait(&tready[s], (uint32_t)(j / NST) & 1u);   // this stage's digit tiles
+        c_tready += OWQ_CLK() - t1;
+        if (kTrace && p.trace && dq == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 224 + kst] = gtime();
         tc_fence_after();
         const uint32_t stile = ring0 + (uint32_t)s * (uint32_t)p.stage_bytes;
         const bool cont = (dsc.flags & kGroupCont) != 0;   // the stage's last group continues in the next stage
@@ -843,9 +793,9 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
         } else if (!p.g.group && hi - lo == C::kIPW) {
           // common case: one scale group, full share -> one asm block, one elect
           const uint32_t dbuf = dcnt & 1u;
-          const long long td0 = clock64();
+          const long long td0 = OWQ_CLK();
           if (!open && dcnt >= 2) mbar_wait(&dempty[dq * 2 + dbuf], ((dcnt >> 1) - 1) & 1u);
-          c_dempty += clock64() - td0;
+          c_dempty += OWQ_CLK() - td0;
           tc_mma_i8_stage<C::kIPW, NN * kSuperStep, kLbo>(
               tmem + (uint32_t)(C::kDCol0 + (dq * 2 + dbuf) * C::kGP * NN), a_wg + buf * (uint32_t)C::kABuf,
               umma_desc(stile + (uint32_t)lo * tile_bytes, kLbo, 128), idesc_i8<NN>(), open ? 1u : 0u);
@@ -880,13 +830,13 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
             pa = sg.pb + 1;
           }
         }
-        const long long t2 = clock64();
+        const long long t2 = OWQ_CLK();
         tc_commit_elect(&aempty[wg * 2 + buf]);   // A buffer consumed once these MMAs complete
         tc_commit_elect(&empty[s]);                // ... and the stage's digit tiles
-        const long long t3 = clock64();
+        const long long t3 = OWQ_CLK();
         c_issue += t2 - t1;
         c_commit += t3 - t2;
-        if (p.trace && dq == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
+        if (kTrace && p.trace && dq == 0 && lane == 0 && kst < 32) p.trace[cta * 256 + 128 + kst] = gtime();
         ++kst;
       } else if (open) {
         // the other issuer's stage: does my open group end inside it?
@@ -902,7 +852,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       ++j;
     }
     if (open && !(C::kGP > 1 && p.g.group)) close_group();
-    if (p.trace && lane == 0) {
+    if (kTrace && p.trace && lane == 0) {
       p.trace[cta * 256 + 1 + dq] = (unsigned long long)c_wait;
       p.trace[cta * 256 + 5 + dq] = (unsigned long long)c_issue;
       p.trace[cta * 256 + 9 + dq * 0] = (unsigned long long)c_commit;
@@ -987,7 +937,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
         // the stage's digit sums and (s, z) blocks are staged in the ring (tready / full)
         const int rs = jc % NST;
         const uint32_t rph = (uint32_t)(jc / NST) & 1u;
-        long long tq0 = clock64();
+        long long tq0 = OWQ_CLK();
         if (q == 0) {
           mbar_wait(&full[rs], rph);
           mbar_wait(&tready[rs], rph);
@@ -995,21 +945,21 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
         named_sync(2, 128);
         const uint32_t sb = smem_addr(ring + (size_t)rs * p.stage_bytes);
         (void)kCapMax;
-        long long tq1 = clock64();
+        long long tq1 = OWQ_CLK();
         e_ring += tq1 - tq0;
         for (int w = 0; w < DWG; ++w) {
-          long long tw0 = clock64();
+          long long tw0 = OWQ_CLK();
           if (q == 0) mbar_wait(&dfull[w * 2 + (jc & 1)], ((uint32_t)jc >> 1) & 1u);
           named_sync(2, 128);
           tc_fence_after();
-          long long tw1 = clock64();
+          long long tw1 = OWQ_CLK();
           e_dfull += tw1 - tw0;
           int lo, hi;
           share<DWG>(cn, w, lo, hi);
           if (lo < hi) {
             const uint32_t tcol = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(C::kDCol0 + (w * 2 + (jc & 1)) * C::kGP * NN);
             const int g0 = (cli + lo) >> gl;
-            long long tw2 = clock64();
+            long long tw2 = OWQ_CLK();
 #pragma unroll
             for (int c16 = 0; c16 < C::kGP * NN / 16; ++c16) {   // two pieces (2 x NN columns) per load
               uint32_t dd[16];
@@ -1042,7 +992,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
                 }
               }
             }
-            e_comb += clock64() - tw2;
+            e_comb += OWQ_CLK() - tw2;
           }
           tc_fence_before();
           __syncwarp();
@@ -1110,7 +1060,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
             }
           }
           if (ends) {
-            if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 18 + 6 * ngend] = gtime();
+            if (kTrace && p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 18 + 6 * ngend] = gtime();
             // block-reduce the digit-sum shares (the same for every row)
             long long S[MAXB];
             if (sdirect) {
@@ -1133,7 +1083,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
                 S[b] = rd[b] + rd[OWQ_MAX_BATCH + b] + rd[2 * OWQ_MAX_BATCH + b] + rd[3 * OWQ_MAX_BATCH + b];
               ++rr;
             }
-            if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 19 + 6 * ngend] = gtime();
+            if (kTrace && p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 19 + 6 * ngend] = gtime();
             const __half2 szv = u2h(szw);
             const float s_g = __low2float(szv);
             const double z_g = (double)__high2float(szv);
@@ -1184,11 +1134,11 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
                 ++dcnt[w];
               }
             }
-            if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 20 + 6 * ngend] = gtime();
+            if (kTrace && p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 20 + 6 * ngend] = gtime();
 #pragma unroll
             for (int b = 0; b < MAXB; ++b)
               tot[b] = fmaf(s_g, (float)((dacc[b] - z_g * (double)S[b]) * 5.9604644775390625e-08), tot[b]);
-            if (p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 21 + 6 * ngend] = gtime();
+            if (kTrace && p.trace && et == 0 && ngend < 4) p.trace[cta * 256 + 21 + 6 * ngend] = gtime();
             ++ngend;
             part = 0;
             gopen = false;
@@ -1255,13 +1205,13 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           }
         }
       }
-      if (p.trace && et == 0 && kst < 32) p.trace[cta * 256 + 160 + kst] = gtime();
+      if (kTrace && p.trace && et == 0 && kst < 32) p.trace[cta * 256 + 160 + kst] = gtime();
       ++kst;
 
       if (gmode && (nn == 0 || nrb != crb || nli >= g.nss)) OWQ_GM_FINISH();   // the row-block's code part is done
       if (nn == 0 || nrb != crb) {
         // -------------------------------------------------- finish row-block crb
-        if (p.trace && et == 0) p.trace[cta * 256 + 50] = gtime();
+        if (kTrace && p.trace && et == 0) p.trace[cta * 256 + 50] = gtime();
         const int64_t ifirst = crb * n_rb, ilast = ifirst + n_rb - 1;
         const bool whole = ifirst >= i0 && ilast < i1;
         const int64_t grow = crb * kRowBlock + row;
@@ -1353,13 +1303,13 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
         }
 #pragma unroll
         for (int b = 0; b < MAXB; ++b) tot[b] = 0.f;
-        if (p.trace && et == 0) p.trace[cta * 256 + 56] = gtime();
+        if (kTrace && p.trace && et == 0) p.trace[cta * 256 + 56] = gtime();
       }
       crb = nrb;
       cli = nli;
       cn = nn;
     }
-    if (p.trace && et == 0) {
+    if (kTrace && p.trace && et == 0) {
       p.trace[cta * 256 + 53] = (unsigned long long)e_ring;
       p.trace[cta * 256 + 54] = (unsigned long long)e_dfull;
       p.trace[cta * 256 + 55] = (unsigned long long)e_ld;
@@ -1373,7 +1323,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
   }
-  if (p.trace && threadIdx.x == 0) p.trace[cta * 256 + 62] = gtime();
+  if (kTrace && p.trace && threadIdx.x == 0) p.trace[cta * 256 + 62] = gtime();
 }
 
 // Device inverse of the code layout (test hook): one CTA (128 threads = rows) per
@@ -1419,37 +1369,66 @@ static int64_t grid_for(const Geo& g, int grid) {
   return G < cap ? G : cap;
 }
 
-static owq_status check_blob(const owq_shape* s, const void* d_packed, Geo& g) {
+// ---- blob registry: which layout a device blob holds, verified once ------------
+// owq_pack registers the blobs it writes; any other blob pointer is verified
+// once by reading its header (one device -> host copy on the call's stream),
+// then remembered.  Keyed by (pointer, shape): a pointer reused for a blob of
+// another shape misses and is re-read.  Unbounded (one entry per packed layer;
+// OPT-175B has 576), process-wide, mutex-protected.
+struct RegKey {
+  const void* p;
+  owq_shape s;
+  bool operator==(const RegKey& o) const { return p == o.p && !std::memcmp(&s, &o.s, sizeof(owq_shape)); }
+};
+struct RegHash {
+  size_t operator()(const RegKey& k) const {
+    size_t h = std::hash<const void*>()(k.p);
+    const int32_t* v = &k.s.c_out;
+    for (int i = 0; i < 5; ++i) h = h * 1000003u ^ (size_t)(uint32_t)v[i];
+    return h;
+  }
+};
+static std::mutex g_reg_mu;
+static std::unordered_map<RegKey, int, RegHash> g_reg;   // -> layout (3 or 4)
+
+void register_blob(const owq_shape* s, const void* d_packed, int layout) {
+  std::lock_guard<std::mutex> lk(g_reg_mu);
+  g_reg[RegKey{d_packed, *s}] = layout;
+}
+
+// Layout of a device blob that must hold `s`: 3 or 4, or an error status (< 0 never: see out).
+static owq_status blob_layout(const owq_shape* s, const void* d_packed, cudaStream_t stream, int& layout) {
   if (!s || !d_packed) return OWQ_ERR_INVALID_ARG;
   if (owq_packed_bytes(s) == 0) return OWQ_ERR_UNSUPPORTED;
   if (reinterpret_cast<uintptr_t>(d_packed) & 15) return OWQ_ERR_INVALID_ARG;
-  BlobHeader h;
-  if (cudaMemcpy(&h, d_packed, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return OWQ_ERR_CUDA;
-  if (h.magic != kMagic || h.version != OWQ_LAYOUT_VERSION || h.M != s->c_out || h.K != s->c_in ||
-      h.bits != s->bits || h.group != s->group_size || h.k != s->n_weak)
-    return OWQ_ERR_BAD_BLOB;
-  g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
-  return OWQ_OK;
-}
-
-// Header checks cost a device->host copy; cache verified blob pointers per shape
-// so the hot path does not synchronise (the blob is immutable).
-struct BlobCacheEntry { const void* ptr; owq_shape s; };
-static thread_local BlobCacheEntry g_blob_cache[16];
-static thread_local int g_blob_cache_next = 0;
-
-static owq_status check_blob_cached(const owq_shape* s, const void* d_packed, Geo& g) {
-  for (auto& e : g_blob_cache)
-    if (e.ptr == d_packed && std::memcmp(&e.s, s, sizeof(owq_shape)) == 0) {
-      g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
-      return OWQ_OK;
-    }
-  owq_status st = check_blob(s, d_packed, g);
-  if (st == OWQ_OK) {
-    g_blob_cache[g_blob_cache_next] = {d_packed, *s};
-    g_blob_cache_next = (g_blob_cache_next + 1) % 16;
+  {
+    std::lock_guard<std::mutex> lk(g_reg_mu);
+    auto it = g_reg.find(RegKey{d_packed, *s});
+    if (it != g_reg.end()) { layout = it->second; return OWQ_OK; }
   }
-  return st;
+  uint8_t hb[64];
+  if (cudaMemcpyAsync(hb, d_packed, sizeof(hb), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
+      cudaStreamSynchronize(stream) != cudaSuccess)
+    return OWQ_ERR_CUDA;
+  uint32_t mv[2];
+  std::memcpy(mv, hb, 8);
+  if (mv[0] == kMagic && mv[1] == OWQ_LAYOUT_VERSION) {
+    BlobHeader h;
+    std::memcpy(&h, hb, sizeof(h));
+    if (h.M != s->c_out || h.K != s->c_in || h.bits != s->bits || h.group != s->group_size || h.k != s->n_weak)
+      return OWQ_ERR_BAD_BLOB;
+    layout = OWQ_LAYOUT_VERSION;
+  } else if (mv[0] == cc::kMagic && mv[1] == (uint32_t)OWQ_LAYOUT_CC) {
+    cc::BlobHeader h;
+    std::memcpy(&h, hb, sizeof(h));
+    if (h.M != s->c_out || h.K != s->c_in || h.bits != s->bits || h.group != s->group_size || h.k != s->n_weak)
+      return OWQ_ERR_BAD_BLOB;
+    layout = OWQ_LAYOUT_CC;
+  } else {
+    return OWQ_ERR_BAD_BLOB;
+  }
+  register_blob(s, d_packed, layout);
+  return OWQ_OK;
 }
 
 // Workspace: [counters nrb u32][partials (nrb + grid) x B x 128 f32]
@@ -1485,8 +1464,8 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   const int64_t avail = (int64_t)maxsmem - (int64_t)fixed - 1024;
   // items per warpgroup per stage: fill the TMEM A buffers, but keep >= 4 stages
   const int64_t per_item = std::max<int64_t>(p.g.ss_bytes, kWeakChunkBytes) + tile_bytes +
-                           (C::kInDig ? p.Bp * 8 + p.B * kSuperStep * 2 : 0);
-  static const int ipw_env = getenv("OWQ_IPW") ? atoi(getenv("OWQ_IPW")) : 0;   // experiments
+                           0;
+  static const int ipw_env = knob("OWQ_IPW", 0);
   int ipw = ipw_env > 0 && ipw_env < C::kIPW ? ipw_env : C::kIPW;
   while (ipw > 1 && 4 * (C::DWG * ipw * per_item + 2048) > avail) --ipw;
   p.cap = C::DWG * ipw;
@@ -1494,12 +1473,12 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   p.tile_off = p.code_bytes;
   p.sum_off = p.tile_off + (int32_t)(p.cap * tile_bytes);
   p.gstage = (C::kGP > 1 && p.g.group) ? 1 : 0;
-  p.x_off = p.sum_off + (int32_t)(((C::kInDig || p.gstage) ? p.cap * p.Bp * 8 : 0) + 127) / 128 * 128;
-  p.sz_off = p.x_off + (int32_t)((C::kInDig ? p.B * p.cap * kSuperStep * 2 : 0) + 127) / 128 * 128;
+  p.x_off = p.sum_off + (int32_t)((p.gstage ? p.cap * p.Bp * 8 : 0) + 127) / 128 * 128;
+  p.sz_off = p.x_off;
   const int sz_blocks = p.gstage ? (int)(p.cap * kSuperStep / p.g.group + 2) : 0;
   p.stage_bytes = (int32_t)((p.sz_off + sz_blocks * kSZBlockBytes + 127) / 128 * 128);
   int nst = (int)(avail / (p.stage_bytes + 32));
-  static const int max_nst = getenv("OWQ_NST") ? atoi(getenv("OWQ_NST")) : 8;
+  static const int max_nst = knob("OWQ_NST", 8);
   nst = std::min(nst, max_nst);
   if (nst < 2) return OWQ_ERR_UNSUPPORTED;     // too many weak columns / batch rows for shared memory
   p.nst = nst;
@@ -1511,7 +1490,7 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
       return OWQ_ERR_CUDA;
     configured = smem;
   }
-  static const int pdl = getenv("OWQ_PDL") ? atoi(getenv("OWQ_PDL")) : 2;   // experiments: 0 off, 1 GEMV, 2 both
+  static const int pdl = knob("OWQ_PDL", 2);   // 0 off, 1 GEMV, 2 both
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1534,7 +1513,7 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
 
 template <int BITS>
 static owq_status launch_n(const Params& p, int64_t grid, cudaStream_t cs) {
-  static const int dwg = getenv("OWQ_DWG") ? atoi(getenv("OWQ_DWG")) : 0;   // experiments (B = 1 only)
+  static const int dwg = knob("OWQ_DWG", 0);   // B = 1 only
   switch (mma_n_for(p.B)) {
     case 8:   // batch 1: 2 decode warpgroups x 6 items measured best (fewer TMEM stores racing the MMAs)
       if (dwg == 3) return launch<BITS, 8, 3>(p, grid, cs);
@@ -1552,9 +1531,13 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
                             int y_f32, void* d_ws, size_t ws_bytes, int grid_req, void* stream) {
   if (!d_x || !d_y || !d_ws) return OWQ_ERR_INVALID_ARG;
   if (B < 1 || B > OWQ_MAX_BATCH) return OWQ_ERR_UNSUPPORTED;
-  Geo g;
-  owq_status st = check_blob_cached(s, d_packed, g);
+  int layout = 0;
+  owq_status st = blob_layout(s, d_packed, (cudaStream_t)stream, layout);
   if (st != OWQ_OK) return st;
+  if (layout == OWQ_LAYOUT_CC)
+    return cc::gemm(cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak), d_packed, d_x, B, d_y, y_f32,
+                    d_ws, ws_bytes, grid_req, (cudaStream_t)stream);
+  const Geo g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
   const int64_t grid = grid_for(g, grid_req);
   if (grid > kMaxGrid || (int64_t)g.nrb * items_per_rb(g) >= (1ll << 31)) return OWQ_ERR_UNSUPPORTED;
   if (ws_bytes < ws_bytes_for(g, B, grid)) return OWQ_ERR_BUFFER_TOO_SMALL;
@@ -1622,20 +1605,10 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   p.y_f32 = y_f32 ? 1 : 0;
   p.xK = g.K;
   cudaStream_t cs = (cudaStream_t)stream;
-  if (false) {   // in-kernel digit mode only (off): TMA of x needs 16-byte aligned rows
-    // in-kernel digit mode streams x with TMA: rows must be 16-byte aligned
-    __half* xp = (__half*)((uint8_t*)d_ws + ws_sync() + ws_counters(g) + ws_partials(g, B, grid) + ws_tiles(g, B) + ws_sums(g, B));
-    const int Kp = g.nss * kSuperStep;
-    const int64_t n = (int64_t)B * Kp;
-    owq_pad_x_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, cs>>>(p.x, xp, B, g.K, Kp);
-    if (cudaGetLastError() != cudaSuccess) return OWQ_ERR_CUDA;
-    p.x = xp;
-    p.xK = Kp;
-  }
   // x -> exact int8 digits in UMMA tile order, plus per-super-step digit sums
-  static const int skip = getenv("OWQ_SKIP") ? atoi(getenv("OWQ_SKIP")) : 0;   // experiments: 1 no digit pass, 2 no GEMV
+  static const int skip = knob("OWQ_SKIP", 0);   // 1 no digit pass, 2 no GEMV (timing experiments)
   if (skip != 1) {
-    static const int pdl = getenv("OWQ_PDL") ? atoi(getenv("OWQ_PDL")) : 2;
+    static const int pdl = knob("OWQ_PDL", 2);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1655,8 +1628,13 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   // experiments only: OWQ_TRACE=<file> appends each call's per-CTA stamps to the
   // file; with OWQ_TRACE_DEFER set, calls only record (graph-capturable) and
   // owq_debug_trace_dump() writes the last launch's stamps.
+#ifdef OWQ_EXPERIMENTS
   static const char* trace_path = getenv("OWQ_TRACE");
   static const bool trace_defer = getenv("OWQ_TRACE_DEFER") != nullptr;
+#else
+  static const char* trace_path = nullptr;
+  static const bool trace_defer = false;
+#endif
   if (trace_path && !g_trace_buf) {
     cudaMalloc(&g_trace_buf, 4096 * 256 * 8);
     cudaMemset(g_trace_buf, 0, 4096 * 256 * 8);
@@ -1665,7 +1643,7 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
   if (trace_buf) cudaMemsetAsync(trace_buf, 0, 4096 * 256 * 8, cs);
   p.trace = g_trace_buf;
   g_trace_grid = grid;
-  static const int exp_env = getenv("OWQ_EXP") ? atoi(getenv("OWQ_EXP")) : 0;
+  static const int exp_env = knob("OWQ_EXP", 0);
   p.exp = exp_env;
 
   p.group_log2 = 0;
@@ -1703,33 +1681,46 @@ extern "C" {
 owq_status owq_pack(const owq_shape* s, const owq_host_layer* L, int flags, void* d_packed, size_t d_bytes,
                     void* stream) {
   if (!d_packed) return OWQ_ERR_INVALID_ARG;
-  const size_t n = owq_packed_bytes(s);
+  const int layout = (flags & OWQ_PACK_LAYOUT_CC) ? OWQ_LAYOUT_CC : OWQ_LAYOUT_VERSION;
+  const size_t n = owq_packed_bytes_layout(s, layout);
   if (n == 0) return OWQ_ERR_UNSUPPORTED;
   if (d_bytes < n) return OWQ_ERR_BUFFER_TOO_SMALL;
+  if (reinterpret_cast<uintptr_t>(d_packed) & 15) return OWQ_ERR_INVALID_ARG;
   std::vector<uint8_t> host(n);
   owq_status st = owq_pack_host(s, L, flags, host.data(), n);
   if (st != OWQ_OK) return st;
   cudaStream_t cs = (cudaStream_t)stream;
   if (cudaMemcpyAsync(d_packed, host.data(), n, cudaMemcpyHostToDevice, cs) != cudaSuccess) return OWQ_ERR_CUDA;
   if (cudaStreamSynchronize(cs) != cudaSuccess) return OWQ_ERR_CUDA;
+  register_blob(s, d_packed, layout);
   return OWQ_OK;
 }
 
 owq_status owq_unpack_codes(const owq_shape* s, const void* d_packed, uint8_t* d_codes, void* stream) {
   if (!d_codes) return OWQ_ERR_INVALID_ARG;
-  Geo g;
-  owq_status st = check_blob(s, d_packed, g);
+  int layout = 0;
+  owq_status st = blob_layout(s, d_packed, (cudaStream_t)stream, layout);
   if (st != OWQ_OK) return st;
+  if (layout == OWQ_LAYOUT_CC)
+    return cc::unpack(cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak), d_packed, d_codes,
+                      (cudaStream_t)stream);
+  const Geo g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
   owq_unpack_codes_kernel<<<(unsigned)((int64_t)g.nrb * g.nss), kRowBlock, 0, (cudaStream_t)stream>>>(
       (const uint8_t*)d_packed, g, d_codes);
   return cudaGetLastError() == cudaSuccess ? OWQ_OK : OWQ_ERR_CUDA;
 }
 
-size_t owq_workspace_bytes(const owq_shape* s, int batch) {
-  if (owq_packed_bytes(s) == 0 || batch < 1 || batch > OWQ_MAX_BATCH) return 0;
-  Geo g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
-  return ws_bytes_for(g, batch, device_sms());   // any k and the default grid fit
+size_t owq_workspace_bytes_grid(const owq_shape* s, int batch, int grid) {
+  if (owq_packed_bytes(s) == 0 || batch < 1 || batch > OWQ_MAX_BATCH || grid < 0) return 0;
+  const Geo g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
+  // an upper bound for any n_weak: the requested grid before the per-shape cap
+  const int64_t G = grid > 0 ? grid : device_sms();
+  if (G > kMaxGrid) return 0;
+  // one workspace serves either layout of the layer
+  return std::max(ws_bytes_for(g, batch, G), cc::workspace_bytes((int)G, std::min(batch, 4)));
 }
+
+size_t owq_workspace_bytes(const owq_shape* s, int batch) { return owq_workspace_bytes_grid(s, batch, 0); }
 
 owq_status owq_gemv(const owq_shape* s, const void* d_packed, const uint16_t* d_x, void* d_y, int y_f32, void* d_ws,
                     size_t ws_bytes, void* stream) {

@@ -11,6 +11,7 @@
 
 #include "owq.h"
 #include "owq_layout.h"
+#include "owq_layout_cc.h"
 
 using owq::Geo;
 
@@ -181,6 +182,107 @@ void write_blob(const Layer& L, uint8_t* blob) {
   for (int t = 0; t < L.k; ++t) std::memcpy(blob + g.widx_off + 2 * t, &L.widx[t], 2);
 }
 
+// Layout version 4 (owq_layout_cc.h): items of 128 rows x 32 columns for the
+// CUDA-core GEMV; codes placed so that each is one LOP3 away from an fp32
+// subnormal (bit offset p(j) + bits <= 24 inside the register it is read from).
+void write_blob_cc(const Layer& L, uint8_t* blob) {
+  namespace C = owq::cc;
+  const C::Geo g = C::make_geo(L.M, L.K, L.bits, L.group, L.k);
+  std::memset(blob, 0, (size_t)g.total);
+  C::BlobHeader h{};
+  h.magic = C::kMagic; h.version = C::kVersion;
+  h.M = L.M; h.K = L.K; h.bits = L.bits; h.group = L.group; h.k = L.k;
+  h.nrb = g.nrb; h.nsteps = g.nsteps; h.kpad = g.kpad; h.G = g.G; h.W = g.W; h.total = g.total;
+  std::memcpy(blob, &h, sizeof(h));
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int rb = 0; rb < g.nrb; ++rb) {
+    for (int st = 0; st < g.nsteps; ++st) {
+      uint8_t* it = blob + g.units_off + C::item_offset(g, rb, st);
+      for (int rr = 0; rr < C::kRowBlock; ++rr) {
+        const int row = rb * C::kRowBlock + rr;
+        if (row >= L.M) continue;
+        uint32_t words[4] = {0, 0, 0, 0};
+        for (int j = 0; j < C::kStep; ++j) {
+          const int col = st * C::kStep + j;
+          const uint32_t code = col < L.K ? L.codes[(size_t)row * L.K + col] : 0u;
+          for (int bit = 0; bit < L.bits; ++bit) {
+            if (!((code >> bit) & 1u)) continue;
+            int word, pos;
+            C::cc_bit_loc(L.bits, j, bit, word, pos);
+            words[word] |= 1u << pos;
+          }
+        }
+        const int lane = rr >> 2, r = rr & 3;
+        for (int c = 0; c < g.W; ++c) std::memcpy(it + (c * 32 + lane) * 16 + r * 4, &words[c], 4);
+      }
+    }
+    for (int gi = 0; gi < g.G; ++gi) {
+      uint8_t* sz = blob + g.sz_off + ((int64_t)rb * g.G + gi) * C::kSZBlockBytes;
+      for (int rr = 0; rr < C::kRowBlock; ++rr) {
+        const int row = rb * C::kRowBlock + rr;
+        uint16_t pair[2] = {0, 0};
+        if (row < L.M) { pair[0] = L.scale[(size_t)row * g.G + gi]; pair[1] = L.zero[(size_t)row * g.G + gi]; }
+        std::memcpy(sz + 4 * rr, pair, 4);
+      }
+    }
+    uint8_t* weak = blob + g.weak_off + (int64_t)rb * g.weak_rb_bytes;
+    for (int t = 0; t < L.k; ++t)
+      for (int rr = 0; rr < C::kRowBlock; ++rr) {
+        const int row = rb * C::kRowBlock + rr;
+        const uint16_t v = row < L.M ? L.wval[(size_t)row * L.k + t] : 0;
+        std::memcpy(weak + (int64_t)(t / C::kWeakChunk) * C::kWeakChunkBytes + (rr * C::kWeakChunk + t % C::kWeakChunk) * 2, &v, 2);
+      }
+  }
+  uint32_t* mask = reinterpret_cast<uint32_t*>(blob + g.wmask_off);
+  for (int t = 0; t < L.k; ++t) {
+    std::memcpy(blob + g.widx_off + 2 * t, &L.widx[t], 2);
+    mask[L.widx[t] >> 5] |= 1u << (L.widx[t] & 31);
+  }
+}
+
+owq_status decode_cc(const void* h_blob, size_t bytes, owq_shape* shape_out, uint8_t* codes, uint16_t* scale,
+                     uint16_t* zero, uint16_t* weak_idx, uint16_t* weak_val) {
+  namespace C = owq::cc;
+  C::BlobHeader h;
+  std::memcpy(&h, h_blob, sizeof(h));
+  owq_shape s{h.M, h.K, h.bits, h.group, h.k};
+  if (!shape_ok(&s)) return OWQ_ERR_BAD_BLOB;
+  const C::Geo g = C::make_geo(h.M, h.K, h.bits, h.group, h.k);
+  if ((size_t)g.total > bytes || g.total != h.total) return OWQ_ERR_BAD_BLOB;
+  const uint8_t* blob = (const uint8_t*)h_blob;
+  if (shape_out) *shape_out = s;
+  for (int row = 0; row < h.M; ++row) {
+    const int rb = row / C::kRowBlock, rr = row % C::kRowBlock, lane = rr >> 2, r = rr & 3;
+    if (codes)
+      for (int col = 0; col < h.K; ++col) {
+        const uint8_t* it = blob + g.units_off + C::item_offset(g, rb, col / C::kStep);
+        uint32_t c = 0;
+        for (int bit = 0; bit < h.bits; ++bit) {
+          int word, pos;
+          C::cc_bit_loc(h.bits, col % C::kStep, bit, word, pos);
+          uint32_t v;
+          std::memcpy(&v, it + (word * 32 + lane) * 16 + r * 4, 4);
+          c |= ((v >> pos) & 1u) << bit;
+        }
+        codes[(size_t)row * h.K + col] = (uint8_t)c;
+      }
+    for (int gi = 0; gi < g.G; ++gi) {
+      uint16_t pair[2];
+      std::memcpy(pair, blob + g.sz_off + ((int64_t)rb * g.G + gi) * C::kSZBlockBytes + 4 * rr, 4);
+      if (scale) scale[(size_t)row * g.G + gi] = pair[0];
+      if (zero) zero[(size_t)row * g.G + gi] = pair[1];
+    }
+    if (weak_val)
+      for (int t = 0; t < h.k; ++t)
+        std::memcpy(&weak_val[(size_t)row * h.k + t],
+                    blob + g.weak_off + (int64_t)rb * g.weak_rb_bytes + (int64_t)(t / C::kWeakChunk) * C::kWeakChunkBytes +
+                        (rr * C::kWeakChunk + t % C::kWeakChunk) * 2, 2);
+  }
+  if (weak_idx)
+    for (int t = 0; t < h.k; ++t) std::memcpy(&weak_idx[t], blob + g.widx_off + 2 * t, 2);
+  return OWQ_OK;
+}
+
 owq_status read_header(const void* h_blob, size_t bytes, owq::BlobHeader& h, Geo& g) {
   if (!h_blob || bytes < (size_t)owq::kHeaderBytes) return OWQ_ERR_INVALID_ARG;
   std::memcpy(&h, h_blob, sizeof(h));
@@ -273,20 +375,35 @@ size_t owq_packed_bytes(const owq_shape* s) {
   return (size_t)owq::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak).total;
 }
 
+size_t owq_packed_bytes_layout(const owq_shape* s, int layout) {
+  if (!shape_ok(s)) return 0;
+  if (layout == OWQ_LAYOUT_VERSION) return owq_packed_bytes(s);
+  if (layout == OWQ_LAYOUT_CC) return (size_t)owq::cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak).total;
+  return 0;
+}
+
 owq_status owq_pack_host(const owq_shape* s, const owq_host_layer* L, int flags, void* h_blob,
                          size_t blob_bytes) {
   if (!h_blob) return OWQ_ERR_INVALID_ARG;
   Layer lay;
   owq_status st = load_layer(s, L, flags, lay);
   if (st != OWQ_OK) return st;
-  if (blob_bytes < owq_packed_bytes(s)) return OWQ_ERR_BUFFER_TOO_SMALL;
-  write_blob(lay, (uint8_t*)h_blob);
+  const bool cc = flags & OWQ_PACK_LAYOUT_CC;
+  if (blob_bytes < owq_packed_bytes_layout(s, cc ? OWQ_LAYOUT_CC : OWQ_LAYOUT_VERSION)) return OWQ_ERR_BUFFER_TOO_SMALL;
+  if (cc) write_blob_cc(lay, (uint8_t*)h_blob);
+  else write_blob(lay, (uint8_t*)h_blob);
   return OWQ_OK;
 }
 
 owq_status owq_blob_decode_host(const void* h_blob, size_t bytes, owq_shape* shape_out,
                                 uint8_t* codes, uint16_t* scale, uint16_t* zero,
                                 uint16_t* weak_idx, uint16_t* weak_val) {
+  if (h_blob && bytes >= (size_t)owq::kHeaderBytes) {
+    uint32_t mv[2];
+    std::memcpy(mv, h_blob, 8);
+    if (mv[0] == owq::cc::kMagic && mv[1] == (uint32_t)OWQ_LAYOUT_CC)
+      return decode_cc(h_blob, bytes, shape_out, codes, scale, zero, weak_idx, weak_val);
+  }
   owq::BlobHeader h;
   Geo g;
   owq_status st = read_header(h_blob, bytes, h, g);
@@ -362,8 +479,10 @@ owq_status owq_tp_shard_host(const owq_shape* full, const owq_host_layer* FL, in
   int32_t off;
   owq_status st = slice_layer(full, FL, mode, world, rank, flags, L, sc, zr, wi, wv, ss, off);
   if (st != OWQ_OK) return st;
-  if (blob_bytes < owq_packed_bytes(&ss)) return OWQ_ERR_BUFFER_TOO_SMALL;
-  write_blob(L, (uint8_t*)h_blob);
+  const bool cc = flags & OWQ_PACK_LAYOUT_CC;
+  if (blob_bytes < owq_packed_bytes_layout(&ss, cc ? OWQ_LAYOUT_CC : OWQ_LAYOUT_VERSION)) return OWQ_ERR_BUFFER_TOO_SMALL;
+  if (cc) write_blob_cc(L, (uint8_t*)h_blob);
+  else write_blob(L, (uint8_t*)h_blob);
   return OWQ_OK;
 }
 

@@ -99,7 +99,7 @@ owq_status owq_tp_shard(const owq_shape* full, const owq_host_layer* FL, int mod
   owq_shape ss;
   owq_status st = owq_tp_shard_shape(full, FL, mode, world, rank, &ss, nullptr);
   if (st != OWQ_OK) return st;
-  const size_t n = owq_packed_bytes(&ss);
+  const size_t n = owq_packed_bytes_layout(&ss, (flags & OWQ_PACK_LAYOUT_CC) ? OWQ_LAYOUT_CC : OWQ_LAYOUT_VERSION);
   if (d_bytes < n) return OWQ_ERR_BUFFER_TOO_SMALL;
   uint8_t* host = new uint8_t[n];
   st = owq_tp_shard_host(full, FL, mode, world, rank, flags, host, n);

@@ -18,6 +18,12 @@ pytestmark = pytest.mark.gpu
 import paper_2306_02272_b200 as owq  # noqa: E402
 
 
+@pytest.fixture(params=[owq.OWQ_LAYOUT_TC, owq.OWQ_LAYOUT_CC], ids=["tc", "cc"])
+def layout(request):
+    """Both device layouts: 3 = tcgen05 kind::i8 kernel, 4 = CUDA-core FFMA2 kernel."""
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def dev():
     if not torch.cuda.is_available():
@@ -25,8 +31,8 @@ def dev():
     return torch.device("cuda:0")
 
 
-def run(d, x_np, dev, y_f32=True, grid=0):
-    layer = owq.OwqLinear(d, device=dev)
+def run(d, x_np, dev, y_f32=True, grid=0, layout=owq.OWQ_LAYOUT_TC):
+    layer = owq.OwqLinear(d, device=dev, layout=layout)
     x = torch.from_numpy(np.ascontiguousarray(x_np, np.float16)).to(dev)
     if grid:
         y = owq.owq_gemm_small_batch_grid(layer.shape, layer.packed, x, grid, y_f32=y_f32)
@@ -51,11 +57,11 @@ SHAPES = [
 
 
 @pytest.mark.parametrize("M,K,bits,group,k", SHAPES)
-def test_gemv_parity_vs_oracle(dev, M, K, bits, group, k):
+def test_gemv_parity_vs_oracle(dev, layout, M, K, bits, group, k):
     d = synth.representation(M, K, bits, group, k, seed=M * 7 + K)
     rep = rep_from_synth(d)
     x = synth.activations(1, K, seed=K, outliers=d["weak_idx"][:8])
-    y, _ = run(d, x, dev)
+    y, _ = run(d, x, dev, layout=layout)
     y_ref = O.matvec(rep, x.astype(np.float64))
     e, eu = rel_err(y, y_ref)
     assert e <= TOL, (e, eu)
@@ -63,34 +69,34 @@ def test_gemv_parity_vs_oracle(dev, M, K, bits, group, k):
 
 @pytest.mark.parametrize("B", [2, 3, 8, 9, 16])
 @pytest.mark.parametrize("M,K,bits,group,k", [(256, 1024, 4, 128, 4), (300, 700, 3, 0, 11)])
-def test_small_batch_parity(dev, B, M, K, bits, group, k):
+def test_small_batch_parity(dev, layout, B, M, K, bits, group, k):
     d = synth.representation(M, K, bits, group, k, seed=B + M)
     rep = rep_from_synth(d)
     x = synth.activations(B, K, seed=B * 3, outliers=d["weak_idx"])
-    y, _ = run(d, x, dev)
+    y, _ = run(d, x, dev, layout=layout)
     y_ref = O.matvec(rep, x.astype(np.float64))
     assert y.shape == (B, M)
     e, _ = rel_err(y, y_ref)
     assert e <= TOL
 
 
-def test_fp16_output(dev):
+def test_fp16_output(dev, layout):
     d = synth.representation(333, 1500, 3, 0, 7, seed=5)
     x = synth.activations(4, 1500, seed=6, outliers=d["weak_idx"])
-    y16, _ = run(d, x, dev, y_f32=False)
+    y16, _ = run(d, x, dev, y_f32=False, layout=layout)
     y_ref = O.matvec(rep_from_synth(d), x.astype(np.float64))
     e, _ = rel_err(y16, y_ref)
     assert e <= TOL
 
 
-def test_oracle_quantizer_output_config1(dev):
+def test_oracle_quantizer_output_config1(dev, layout):
     # BASELINE config 1 end to end: OWQ quantization by the oracle (768x768, k=8),
     # then the GPU hot path on the oracle's representation.
     W, X, ch = synth.weights_and_calib(768, 768, N=2048, n_outliers=8, seed=2306)
     rep = O.owq_quantize(W, X, 3, 8)
     d = synth_from_rep(rep)
     x = synth.activations(1, 768, seed=2307, outliers=ch)
-    y, layer = run(d, x, dev)
+    y, layer = run(d, x, dev, layout=layout)
     e, _ = rel_err(y, O.matvec(rep, x.astype(np.float64)))
     assert e <= TOL
     # strict packing accepts it (codes of weak columns already equal z)
@@ -98,11 +104,11 @@ def test_oracle_quantizer_output_config1(dev):
 
 
 @pytest.mark.parametrize("bits,group", [(3, 0), (4, 128)])
-def test_device_unpack_bit_exact(dev, bits, group):
+def test_device_unpack_bit_exact(dev, layout, bits, group):
     M, K, k = 200, 1500, 6
     d = synth.representation(M, K, bits, group, k, seed=9)
     shape = owq.Shape(M, K, bits, group, k)
-    packed = owq.owq_pack(shape, d, device=dev)
+    packed = owq.owq_pack(shape, d, device=dev, flags=owq.OWQ_PACK_LAYOUT_CC if layout == owq.OWQ_LAYOUT_CC else 0)
     codes = owq.owq_unpack_codes(shape, packed).cpu().numpy()
     expect = d["codes"].copy()
     z = O.from_fp16_bits(d["zero_f16"]).astype(np.uint8)
@@ -112,13 +118,13 @@ def test_device_unpack_bit_exact(dev, bits, group):
 
 
 @pytest.mark.parametrize("bits,group", [(3, 0), (4, 128)])
-def test_probes_bit_exact(dev, bits, group):
+def test_probes_bit_exact(dev, layout, bits, group):
     # x = e_j: weak j -> y = v[:, t] exactly; non-weak j -> y_i = s_i (q_ij - z_i) exactly
     # (fp16 s times an integer <= 15 is exact in fp32).  Covers index, layout, zero fill.
     M, K, k = 130, 600, 5
     d = synth.representation(M, K, bits, group, k, seed=11)
     rep = rep_from_synth(d)
-    layer = owq.OwqLinear(d, device=dev)
+    layer = owq.OwqLinear(d, device=dev, layout=layout)
     js = list(d["weak_idx"]) + [0, 1, 63, 64, 127, 128, 300, 599]
     X = np.zeros((len(js), K), np.float16)
     for n, j in enumerate(js):
@@ -131,12 +137,12 @@ def test_probes_bit_exact(dev, bits, group):
 
 
 @pytest.mark.parametrize("grid", [1, 2, 3, 7, 13, 64, 500])
-def test_stream_k_any_grid_and_deterministic(dev, grid):
+def test_stream_k_any_grid_and_deterministic(dev, layout, grid):
     M, K, bits, group, k = 700, 5000, 3, 0, 20
     d = synth.representation(M, K, bits, group, k, seed=grid)
     rep = rep_from_synth(d)
     x = synth.activations(2, K, seed=3, outliers=d["weak_idx"])
-    y1, layer = run(d, x, dev, grid=grid)
+    y1, layer = run(d, x, dev, grid=grid, layout=layout)
     e, _ = rel_err(y1, O.matvec(rep, x.astype(np.float64)))
     assert e <= TOL
     xt = torch.from_numpy(x).to(dev)
@@ -146,13 +152,13 @@ def test_stream_k_any_grid_and_deterministic(dev, grid):
 
 
 @pytest.mark.parametrize("M,K,k", [(12288, 12288, 15), (49152, 12288, 3), (12288, 49152, 15)])
-def test_full_size_opt175b_sampled(dev, M, K, k):
+def test_full_size_opt175b_sampled(dev, layout, M, K, k):
     # BASELINE config 5 at full size in the bench launch configuration; the oracle
     # computes a sample of rows one by one (every row-block boundary class covered).
     d = synth.representation(M, K, 3, 0, k, seed=M + K)
     rep = rep_from_synth(d)
     x = synth.activations(1, K, seed=1, outliers=d["weak_idx"][:8])
-    y, _ = run(d, x, dev)
+    y, _ = run(d, x, dev, layout=layout)
     r = np.random.default_rng(0)
     rows = sorted(set([0, 1, 63, 64, M - 1, M - 64] + list(r.choice(M, 120, replace=False))))
     y_ref = O.matvec_rows(rep, x.astype(np.float64), rows)
@@ -184,9 +190,9 @@ def test_tp_world1_nccl(dev):
         owq.owq_tp_destroy(tp)
 
 
-def test_errors_are_loud(dev):
+def test_errors_are_loud(dev, layout):
     d = synth.representation(64, 128, 3, 0, 2, seed=1)
-    layer = owq.OwqLinear(d, device=dev)
+    layer = owq.OwqLinear(d, device=dev, layout=layout)
     x = torch.zeros((17, 128), dtype=torch.float16, device=dev)
     with pytest.raises(owq.OwqError, match="UNSUPPORTED"):
         owq.owq_gemm_small_batch(layer.shape, layer.packed, x)
@@ -207,7 +213,7 @@ def test_back_to_back_graph_shared_workspace(dev):
     for i, (M, K, bits, g, k, B) in enumerate(cases):
         d = synth.representation(M, K, bits, g, k, seed=100 + i)
         x = synth.activations(B, K, seed=200 + i, outliers=d["weak_idx"][:4])
-        L = owq.OwqLinear(d, device=dev)
+        L = owq.OwqLinear(d, device=dev, layout=owq.OWQ_LAYOUT_CC if i % 2 else owq.OWQ_LAYOUT_TC)   # both layouts in one chain
         layers.append(L)
         xs.append(torch.from_numpy(x).to(dev))
         ys.append(torch.empty((B, M), dtype=torch.float32, device=dev))
@@ -289,12 +295,15 @@ def test_workspace_sync_words_left_zero(dev):
     matches the oracle and the fixed synchronisation prefix of the workspace
     (partial-row slots, 0 = not written) is all zero afterwards."""
     cases = [(1000, 700, 3, 0, 11, 1, 0), (4096, 2048, 3, 0, 9, 2, 500), (300, 2000, 4, 128, 7, 1, 0),
-             (2048, 4096, 4, 0, 3, 8, 0), (768, 768, 3, 0, 8, 1, 300), (4096, 1024, 3, 0, 5, 3, 0)]
+             (2048, 4096, 4, 0, 3, 8, 0), (768, 768, 3, 0, 8, 1, 300), (4096, 1024, 3, 0, 5, 3, 0),
+             (1000, 700, 3, 0, 11, 1, -1), (4096, 2048, 4, 128, 9, 2, -700), (768, 768, 3, 0, 8, 4, -3)]
     layers, xs, refs, ws_bytes = [], [], [], 0
     for i, (M, K, bits, g, k, B, grid) in enumerate(cases):
         d = synth.representation(M, K, bits, g, k, seed=300 + i)
         x = synth.activations(B, K, seed=400 + i, outliers=d["weak_idx"][:4])
-        L = owq.OwqLinear(d, device=dev)
+        cc = grid < 0                      # negative grid: the CUDA-core layout at grid |grid| (-1: default)
+        grid = 0 if grid == -1 else abs(grid)
+        L = owq.OwqLinear(d, device=dev, layout=owq.OWQ_LAYOUT_CC if cc else owq.OWQ_LAYOUT_TC)
         layers.append((L, grid))
         xs.append(torch.from_numpy(x).to(dev))
         refs.append(O.matvec(rep_from_synth(d), x.astype(np.float64)))
@@ -314,4 +323,4 @@ def test_workspace_sync_words_left_zero(dev):
             e, _ = rel_err(y.cpu().numpy().astype(np.float64), ref)
             assert e <= TOL
         slots = 512 * 16 * 128 * 4   # kMaxGrid x OWQ_MAX_BATCH x 128 rows x 4 B (owq_gemv.cu ws_sync)
-        assert int(torch.count_nonzero(ws[:slots]).item()) == 0
+        assert int(torch.count_nonzero(ws[:slots]).item()) == 0   # both layouts' slot prefixes

@@ -26,6 +26,25 @@ __device__ __forceinline__ unsigned long long pk(uint32_t lo, uint32_t hi) {
   return ((unsigned long long)hi << 32) | lo;
 }
 
+__device__ __forceinline__ float fhfma_lo(uint32_t a, uint32_t b, float c) {   // fp32 += f16(a.lo) * f16(b.lo)
+  asm volatile("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, al, bl, %0;}" : "+f"(c) : "r"(a), "r"(b));
+  return c;
+}
+__device__ __forceinline__ float fhfma_hi(uint32_t a, uint32_t b, float c) {   // fp32 += f16(a.hi) * f16(b.hi)
+  asm volatile("{.reg .f16 al, ah, bl, bh; mov.b32 {al, ah}, %1; mov.b32 {bl, bh}, %2; fma.rn.f32.f16 %0, ah, bh, %0;}" : "+f"(c) : "r"(a), "r"(b));
+  return c;
+}
+__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm volatile("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t lop_or_and(uint32_t a, uint32_t m, uint32_t magic) {   // (a & m) | magic
+  uint32_t d;
+  asm volatile("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(m), "r"(magic));
+  return d;
+}
+
 // mode 0: LOP3 only (8 independent chains); 1: FFMA2 only; 2: FFMA only;
 // 3: IMAD.HI only; 4: the denormal inner loop (3 words -> 32 codes, 34 ALU,
 // 16 FFMA2 per 32 weights, 4 rows per thread)
@@ -71,6 +90,45 @@ __global__ void probe(uint32_t seed, int iters, unsigned long long* cyc, float* 
       for (int r = 0; r < 8; ++r)
 #pragma unroll
         for (int i = 0; i < 8; ++i) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(w[i]) : "r"(mh), "r"(m[r]));
+    } else if (MODE == 5) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float a = __uint_as_float((uint32_t)acc[i]);
+          a = (r & 1) ? fhfma_hi(w[i], m[r], a) : fhfma_lo(w[i], m[r], a);
+          acc[i] = __float_as_uint(a);
+        }
+    } else if (MODE == 6) {
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = hsub2(w[i], m[r]);
+    } else if (MODE == 7) {
+      // "route M": 4 rows x 10 codes per word, (q - z) 2^p exact in fp16 via the
+      // 1024 magic, products and sums in fp32 with fma.rn.f32.f16 (FHFMA)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t a0 = w[3 * r] ^ it;
+        const uint32_t a1 = a0 >> 9;
+        uint32_t d[5];
+        d[0] = hsub2(lop_or_and(a0, m[0], m[7]), m[4]);
+        d[1] = hsub2(lop_or_and(a0, m[1], m[7]), m[5]);
+        d[2] = hsub2(lop_or_and(a0, m[2], m[7]), m[6]);
+        d[3] = hsub2(lop_or_and(a1, m[0], m[7]), m[4]);
+        d[4] = hsub2(lop_or_and(a1, m[1], m[7]), m[5]);
+        float f0 = __uint_as_float((uint32_t)acc[2 * r]), f1 = __uint_as_float((uint32_t)(acc[2 * r] >> 32));
+        float f2 = __uint_as_float((uint32_t)acc[2 * r + 1]);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+          const uint32_t xv = __float_as_uint(xs[(5 * r + i) & 31]);
+          float& f = i == 0 || i == 3 ? f0 : i == 1 || i == 4 ? f1 : f2;
+          f = fhfma_lo(d[i], xv, f);
+          f = fhfma_hi(d[i], xv, f);
+        }
+        acc[2 * r] = pk(__float_as_uint(f0), __float_as_uint(f1));
+        acc[2 * r + 1] = __float_as_uint(f2);
+      }
     } else {
       // 4 rows x 32 columns: rows in w[3r..3r+2]
 #pragma unroll
@@ -130,10 +188,11 @@ int main() {
   int bad = -1;
   CK(cudaMemcpy(&bad, d_bad, 4, cudaMemcpyDeviceToHost));
   printf("denorm_check: %d mismatches of %d subnormal FFMA2 products\n", bad, 8 * 22 * 1024);
-  const char* names[5] = {"LOP3", "FFMA2", "FFMA", "IMAD.HI", "denormal loop (weights)"};
+  const char* names[8] = {"LOP3", "FFMA2", "FFMA", "IMAD.HI", "denormal loop (weights)", "FHFMA", "HADD2 (f16x2)",
+                          "route M loop (weights)"};
   // ops per thread per iteration
-  const double ops[5] = {64, 64 * 2, 64, 64, 4 * 32};
-  for (int mode = 0; mode < 5; ++mode) {
+  const double ops[8] = {64, 64 * 2, 64, 64, 4 * 32, 64, 64, 4 * 10};
+  for (int mode = 0; mode < 8; ++mode) {
     for (int warps : {8, 16, 32}) {
       const int iters = 2000;
       cudaEvent_t e0, e1;
@@ -144,7 +203,11 @@ int main() {
           case 1: probe<1><<<sms, warps * 32>>>(1u, iters, d_cyc, d_sink); break;
           case 2: probe<2><<<sms, warps * 32>>>(1u, iters, d_cyc, d_sink); break;
           case 3: probe<3><<<sms, warps * 32>>>(1u, iters, d_cyc, d_sink); break;
-          default: probe<4><<<sms, warps * 32>>>(1u, iters, d_cyc, d_sink); break;
+          case 5: probe<5><<<sms, warps * 32>>>(1u, iters, d_cyc, d_sink); break;
+          case 6: probe<6><<<sms, warps * 32>>>(1u, iters, d_cyc, d_sink); break;
+          case 7: probe<7><<<sms, warps * 32>>>(1u, iters, d_cyc, d_sink); break;
+          case 4: probe<4><<<sms, warps * 32>>>(1u, iters, d_cyc, d_sink); break;
+          default: break;
         }
       };
       launch();
