@@ -131,9 +131,46 @@ owq_status owq_pack_host(const owq_shape *shape, const owq_host_layer *layer,
 owq_status owq_pack(const owq_shape *shape, const owq_host_layer *layer,
                     int flags, void *d_packed, size_t d_bytes, void *stream);
 
+/* ---- representation variants (device layout 4 only) ----
+ * act-order: OPTQ quantizes the columns in descending order of
+ * diag(H) and forms its scale groups over that order; storage-favored
+ * (P:486-490): the zero-filled weak columns are not stored at all.  Both are
+ * a code matrix in STORED column order plus a column map: stored position p
+ * holds original column colmap[p].  Scale/zero groups run over stored
+ * positions (G = ceil(k_stored / group_size)); x keeps its c_in columns and
+ * the weak indices stay original column indices.  Stored positions whose
+ * column is weak are zero-filled (reading s10) unless OWQ_PACK_STRICT. */
+typedef struct {
+  int32_t k_stored;          /* stored columns: c_in (latency-favored, a
+                                permutation) or c_in - n_weak (storage-favored) */
+  const uint16_t *colmap;    /* [k_stored] original column of each stored
+                                position; distinct, < c_in                      */
+} owq_colmap;
+
+/* Bytes of the layout-4 blob of `shape` with column map `map`; 0 if invalid. */
+size_t owq_packed_bytes_colmap(const owq_shape *shape, const owq_colmap *map);
+
+/* Pack a column-mapped layer: layer->codes is [c_out][k_stored] in stored
+ * order (canonical stream, or one byte per code with OWQ_PACK_U8_CODES),
+ * scale/zero [c_out][ceil(k_stored / g)], weak_idx/weak_val as in
+ * owq_host_layer.  INVALID_ARG: a colmap entry out of range or repeated. */
+owq_status owq_pack_host_colmap(const owq_shape *shape, const owq_host_layer *layer,
+                                const owq_colmap *map, int flags,
+                                void *h_blob, size_t blob_bytes);
+owq_status owq_pack_colmap(const owq_shape *shape, const owq_host_layer *layer,
+                           const owq_colmap *map, int flags,
+                           void *d_packed, size_t d_bytes, void *stream);
+
+/* Column map of a layout-4 blob (host test hook): *k_stored, and colmap
+ * [k_stored] (identity for blobs packed without a map).  Any output may be NULL. */
+owq_status owq_blob_colmap_host(const void *h_blob, size_t blob_bytes,
+                                int32_t *k_stored, uint16_t *colmap);
+
 /* Host inverse of the packer (test hook): recovers shape, one code per byte
  * [c_out][c_in] (weak columns hold the zero point), fp16 scale/zero [c_out][G],
  * weak_idx [n_weak], weak_val [c_out][n_weak].  Any output pointer may be NULL. */
+/* (for a column-mapped blob, codes come back in stored order, [c_out][k_stored],
+ * and scale/zero [c_out][ceil(k_stored / g)]) */
 owq_status owq_blob_decode_host(const void *h_blob, size_t blob_bytes,
                                 owq_shape *shape_out, uint8_t *codes,
                                 uint16_t *scale, uint16_t *zero,

@@ -26,7 +26,8 @@ __all__ = [
     "owq_tp_shard_shape", "owq_tp_shard_host", "owq_tp_shard", "owq_tp_workspace_bytes",
     "owq_tp_gemv", "OwqLinear", "OWQ_TP_ROWS", "OWQ_TP_COLS", "OWQ_PACK_STRICT",
     "OWQ_PACK_U8_CODES", "OWQ_PACK_LAYOUT_CC", "OWQ_LAYOUT_TC", "OWQ_LAYOUT_CC",
-    "owq_packed_bytes_layout", "owq_workspace_bytes_grid", "EXPORTED_SYMBOLS",
+    "owq_packed_bytes_layout", "owq_workspace_bytes_grid", "owq_packed_bytes_colmap", "owq_pack_host_colmap",
+    "owq_pack_colmap", "owq_blob_colmap_host", "EXPORTED_SYMBOLS",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -42,7 +43,8 @@ EXPORTED_SYMBOLS = [
     "owq_unpack_codes", "owq_workspace_bytes", "owq_workspace_bytes_grid", "owq_gemv", "owq_gemm_small_batch",
     "owq_gemm_small_batch_grid", "owq_tp_get_unique_id", "owq_tp_init", "owq_tp_destroy",
     "owq_tp_shard_shape", "owq_tp_shard_host", "owq_tp_shard", "owq_tp_workspace_bytes",
-    "owq_tp_gemv", "owq_tp_bounds", "owq_status_string",
+    "owq_tp_gemv", "owq_tp_bounds", "owq_status_string", "owq_packed_bytes_colmap",
+    "owq_pack_host_colmap", "owq_pack_colmap", "owq_blob_colmap_host",
 ]
 
 
@@ -60,6 +62,10 @@ class Shape(ctypes.Structure):
 
     def tup(self):
         return (self.c_out, self.c_in, self.bits, self.group_size, self.n_weak)
+
+
+class _ColMap(ctypes.Structure):
+    _fields_ = [("k_stored", ctypes.c_int32), ("colmap", ctypes.c_void_p)]
 
 
 class _HostLayer(ctypes.Structure):
@@ -111,6 +117,10 @@ def lib():
         "owq_tp_gemv": (st, [_P, ctypes.c_int, _S, _S, _P, _P, ctypes.c_int, _P, ctypes.c_int,
                              _P, sz, _P]),
         "owq_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+        "owq_packed_bytes_colmap": (sz, [_S, ctypes.POINTER(_ColMap)]),
+        "owq_pack_host_colmap": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.POINTER(_ColMap), ctypes.c_int, _P, sz]),
+        "owq_pack_colmap": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.POINTER(_ColMap), ctypes.c_int, _P, sz, _P]),
+        "owq_blob_colmap_host": (st, [_P, sz, ctypes.POINTER(ctypes.c_int32), _P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -227,12 +237,64 @@ def owq_pack(shape, rep: dict, flags: int = 0, device=None, stream=None):
     return d
 
 
+def _colmap(colmap):
+    cm = np.ascontiguousarray(colmap, dtype=np.uint16)
+    return _ColMap(int(cm.size), cm.ctypes.data), cm
+
+
+def owq_packed_bytes_colmap(shape, colmap) -> int:
+    m, keep = _colmap(colmap)
+    return int(lib().owq_packed_bytes_colmap(ctypes.byref(_shape(shape)), ctypes.byref(m)))
+
+
+def owq_pack_host_colmap(shape, rep: dict, colmap, flags: int = 0) -> np.ndarray:
+    """NEXT-4 variants (act-order / storage-favored): rep["codes"] is [c_out][k_stored]
+    in stored order, colmap[p] = original column of stored position p."""
+    s = _shape(shape)
+    m, keep = _colmap(colmap)
+    n = int(lib().owq_packed_bytes_colmap(ctypes.byref(s), ctypes.byref(m)))
+    if n == 0:
+        raise OwqError("OWQ_ERR_INVALID_ARG (shape / column map)")
+    blob = np.empty(n, dtype=np.uint8)
+    hl, flags = _layer_from(rep, flags)
+    _check(lib().owq_pack_host_colmap(ctypes.byref(s), ctypes.byref(hl.layer), ctypes.byref(m), flags,
+                                      blob.ctypes.data, n))
+    return blob
+
+
+def owq_pack_colmap(shape, rep: dict, colmap, flags: int = 0, device=None, stream=None):
+    import torch
+    s = _shape(shape)
+    m, keep = _colmap(colmap)
+    n = int(lib().owq_packed_bytes_colmap(ctypes.byref(s), ctypes.byref(m)))
+    if n == 0:
+        raise OwqError("OWQ_ERR_INVALID_ARG (shape / column map)")
+    d = torch.empty(n, dtype=torch.uint8, device=device or "cuda")
+    hl, flags = _layer_from(rep, flags)
+    with torch.cuda.device(d.device):
+        _check(lib().owq_pack_colmap(ctypes.byref(s), ctypes.byref(hl.layer), ctypes.byref(m), flags,
+                                     d.data_ptr(), n, _stream(stream)))
+    return d
+
+
+def owq_blob_colmap_host(blob: np.ndarray):
+    blob = np.ascontiguousarray(blob, dtype=np.uint8)
+    ks = ctypes.c_int32()
+    _check(lib().owq_blob_colmap_host(blob.ctypes.data, blob.size, ctypes.byref(ks), None))
+    cm = np.zeros(ks.value, np.uint16)
+    _check(lib().owq_blob_colmap_host(blob.ctypes.data, blob.size, ctypes.byref(ks), cm.ctypes.data))
+    return cm
+
+
 def owq_blob_decode_host(blob: np.ndarray) -> dict:
     blob = np.ascontiguousarray(blob, dtype=np.uint8)
     s = Shape()
     _check(lib().owq_blob_decode_host(blob.ctypes.data, blob.size, ctypes.byref(s),
                                       None, None, None, None, None))
-    M, K, G = s.c_out, s.c_in, (1 if s.group_size == 0 else -(-s.c_in // s.group_size))
+    M, K = s.c_out, s.c_in
+    if int(blob[:8].view(np.uint32)[1]) == OWQ_LAYOUT_CC:
+        K = owq_blob_colmap_host(blob).size          # stored columns
+    G = 1 if s.group_size == 0 else -(-K // s.group_size)
     out = {"shape": s, "codes": np.zeros((M, K), np.uint8), "scale_f16": np.zeros((M, G), np.uint16),
            "zero_f16": np.zeros((M, G), np.uint16), "weak_idx": np.zeros(s.n_weak, np.uint16),
            "weak_val_f16": np.zeros((M, s.n_weak), np.uint16)}
@@ -440,7 +502,11 @@ class OwqLinear:
         if layout == OWQ_LAYOUT_CC:
             flags |= OWQ_PACK_LAYOUT_CC
         self.layout = layout
-        self.packed = owq_pack(self.shape, rep, flags, device=self.device)
+        if rep.get("colmap") is not None:      # NEXT-4 variants: layout 4 with a column map
+            self.layout = OWQ_LAYOUT_CC
+            self.packed = owq_pack_colmap(self.shape, rep, rep["colmap"], flags, device=self.device)
+        else:
+            self.packed = owq_pack(self.shape, rep, flags, device=self.device)
         self.ws = workspace(self.shape, max_batch, self.device)
 
     @property

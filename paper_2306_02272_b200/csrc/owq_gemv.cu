@@ -1389,22 +1389,23 @@ struct RegHash {
   }
 };
 static std::mutex g_reg_mu;
-static std::unordered_map<RegKey, int, RegHash> g_reg;   // -> layout (3 or 4)
+struct RegVal { int layout, Ks; };   // Ks: stored columns of a column-mapped layout-4 blob, else -1
+static std::unordered_map<RegKey, RegVal, RegHash> g_reg;
 
-void register_blob(const owq_shape* s, const void* d_packed, int layout) {
+void register_blob(const owq_shape* s, const void* d_packed, int layout, int Ks = -1) {
   std::lock_guard<std::mutex> lk(g_reg_mu);
-  g_reg[RegKey{d_packed, *s}] = layout;
+  g_reg[RegKey{d_packed, *s}] = RegVal{layout, Ks};
 }
 
 // Layout of a device blob that must hold `s`: 3 or 4, or an error status (< 0 never: see out).
-static owq_status blob_layout(const owq_shape* s, const void* d_packed, cudaStream_t stream, int& layout) {
+static owq_status blob_layout(const owq_shape* s, const void* d_packed, cudaStream_t stream, int& layout, int& Ks) {
   if (!s || !d_packed) return OWQ_ERR_INVALID_ARG;
   if (owq_packed_bytes(s) == 0) return OWQ_ERR_UNSUPPORTED;
   if (reinterpret_cast<uintptr_t>(d_packed) & 15) return OWQ_ERR_INVALID_ARG;
   {
     std::lock_guard<std::mutex> lk(g_reg_mu);
     auto it = g_reg.find(RegKey{d_packed, *s});
-    if (it != g_reg.end()) { layout = it->second; return OWQ_OK; }
+    if (it != g_reg.end()) { layout = it->second.layout; Ks = it->second.Ks; return OWQ_OK; }
   }
   uint8_t hb[64];
   if (cudaMemcpyAsync(hb, d_packed, sizeof(hb), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
@@ -1423,11 +1424,14 @@ static owq_status blob_layout(const owq_shape* s, const void* d_packed, cudaStre
     std::memcpy(&h, hb, sizeof(h));
     if (h.M != s->c_out || h.K != s->c_in || h.bits != s->bits || h.group != s->group_size || h.k != s->n_weak)
       return OWQ_ERR_BAD_BLOB;
+    if (h.mapped && (h.Ks <= 0 || h.Ks > h.K)) return OWQ_ERR_BAD_BLOB;
     layout = OWQ_LAYOUT_CC;
+    Ks = h.mapped ? h.Ks : -1;
   } else {
     return OWQ_ERR_BAD_BLOB;
   }
-  register_blob(s, d_packed, layout);
+  if (layout != OWQ_LAYOUT_CC) Ks = -1;
+  register_blob(s, d_packed, layout, Ks);
   return OWQ_OK;
 }
 
@@ -1531,12 +1535,12 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
                             int y_f32, void* d_ws, size_t ws_bytes, int grid_req, void* stream) {
   if (!d_x || !d_y || !d_ws) return OWQ_ERR_INVALID_ARG;
   if (B < 1 || B > OWQ_MAX_BATCH) return OWQ_ERR_UNSUPPORTED;
-  int layout = 0;
-  owq_status st = blob_layout(s, d_packed, (cudaStream_t)stream, layout);
+  int layout = 0, Ks = -1;
+  owq_status st = blob_layout(s, d_packed, (cudaStream_t)stream, layout, Ks);
   if (st != OWQ_OK) return st;
   if (layout == OWQ_LAYOUT_CC)
-    return cc::gemm(cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak), d_packed, d_x, B, d_y, y_f32,
-                    d_ws, ws_bytes, grid_req, (cudaStream_t)stream);
+    return cc::gemm(cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak, Ks), d_packed, d_x, B, d_y,
+                    y_f32, d_ws, ws_bytes, grid_req, (cudaStream_t)stream);
   const Geo g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
   const int64_t grid = grid_for(g, grid_req);
   if (grid > kMaxGrid || (int64_t)g.nrb * items_per_rb(g) >= (1ll << 31)) return OWQ_ERR_UNSUPPORTED;
@@ -1696,13 +1700,30 @@ owq_status owq_pack(const owq_shape* s, const owq_host_layer* L, int flags, void
   return OWQ_OK;
 }
 
+owq_status owq_pack_colmap(const owq_shape* s, const owq_host_layer* L, const owq_colmap* map, int flags,
+                           void* d_packed, size_t d_bytes, void* stream) {
+  if (!d_packed) return OWQ_ERR_INVALID_ARG;
+  const size_t n = owq_packed_bytes_colmap(s, map);
+  if (n == 0) return OWQ_ERR_INVALID_ARG;
+  if (d_bytes < n) return OWQ_ERR_BUFFER_TOO_SMALL;
+  if (reinterpret_cast<uintptr_t>(d_packed) & 15) return OWQ_ERR_INVALID_ARG;
+  std::vector<uint8_t> host(n);
+  owq_status st = owq_pack_host_colmap(s, L, map, flags, host.data(), n);
+  if (st != OWQ_OK) return st;
+  cudaStream_t cs = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(d_packed, host.data(), n, cudaMemcpyHostToDevice, cs) != cudaSuccess) return OWQ_ERR_CUDA;
+  if (cudaStreamSynchronize(cs) != cudaSuccess) return OWQ_ERR_CUDA;
+  register_blob(s, d_packed, OWQ_LAYOUT_CC, map->k_stored);
+  return OWQ_OK;
+}
+
 owq_status owq_unpack_codes(const owq_shape* s, const void* d_packed, uint8_t* d_codes, void* stream) {
   if (!d_codes) return OWQ_ERR_INVALID_ARG;
-  int layout = 0;
-  owq_status st = blob_layout(s, d_packed, (cudaStream_t)stream, layout);
+  int layout = 0, Ks = -1;
+  owq_status st = blob_layout(s, d_packed, (cudaStream_t)stream, layout, Ks);
   if (st != OWQ_OK) return st;
   if (layout == OWQ_LAYOUT_CC)
-    return cc::unpack(cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak), d_packed, d_codes,
+    return cc::unpack(cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak, Ks), d_packed, d_codes,
                       (cudaStream_t)stream);
   const Geo g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
   owq_unpack_codes_kernel<<<(unsigned)((int64_t)g.nrb * g.nss), kRowBlock, 0, (cudaStream_t)stream>>>(

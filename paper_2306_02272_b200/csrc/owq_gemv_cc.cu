@@ -245,7 +245,10 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
   using C = Cfg<BITS, NB>;
   constexpr int NW = C::NW, S = C::S, CAP = C::CAP, W = C::W, NST = C::NST;
   constexpr uint32_t ITEM = C::ITEM, STAGE = C::STAGE;
-  constexpr bool XREG = NB <= 2;          // all of x' in registers (else reloaded per row)
+#ifndef OWQ_CC_XREG
+#define OWQ_CC_XREG 2
+#endif
+  constexpr bool XREG = NB <= OWQ_CC_XREG;   // all of x' in registers (else reloaded per row)
   extern __shared__ __align__(128) uint8_t smem[];
   const Geo& g = p.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -402,33 +405,54 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
     }
   };
 
-  auto load_x = [&](XPre<S, NB>& xp, int32_t st, int n) {
+  // column map (NEXT-4 variants): stored position -> original column, loaded
+  // one stage before the x it selects (the x load depends on it)
+  const uint16_t* colmap = g.mapped ? reinterpret_cast<const uint16_t*>(p.blob + g.colmap_off) : nullptr;
+  auto load_j = [&](uint32_t* jq, int32_t st, int n) {
 #pragma unroll
     for (int t = 0; t < S; ++t) {
       const int i = w * S + t;
-      const int64_t col = (int64_t)(st + i) * kStep + lane;
+      const int64_t pos = (int64_t)(st + i) * kStep + lane;
+      jq[t] = (i < n && pos < g.Ks) ? (uint32_t)__ldg(colmap + pos) : 0u;
+    }
+  };
+  auto load_x = [&](XPre<S, NB>& xp, int32_t st, int n, const uint32_t* jq) {
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+      const int i = w * S + t;
+      const int64_t pos = (int64_t)(st + i) * kStep + lane;   // stored position
       xp.m[t] = 0u;
 #pragma unroll
       for (int b = 0; b < NB; ++b) xp.v[t][b] = __ushort_as_half((unsigned short)0);
       if (i < n) {
         xp.m[t] = __ldg(wmask + st + i);
-        if (col < g.K)
+        if (pos < g.Ks) {
+          const int64_t col = colmap ? (int64_t)jq[t] : pos;
 #pragma unroll
           for (int b = 0; b < NB; ++b) xp.v[t][b] = p.x[(int64_t)b * p.xK + col];
+        }
       }
     }
   };
 
-  Walk<CAP> wk, nx;
+  Walk<CAP> wk, nx, nj;
   wk.init(g, u0, u1);
-  nx = wk;                       // two stages ahead (x prefetch)
+  nx = wk;                       // x: two stages ahead; column map: three
   XPre<S, NB> xa_, xb_;
+  uint32_t jq[S];
   {
     int32_t st;
     int n = nx.next_any(st);
-    load_x(xa_, st, n);
+    if (colmap) load_j(jq, st, n);
+    load_x(xa_, st, n, jq);
     n = nx.next_any(st);
-    load_x(xb_, st, n);
+    if (colmap) load_j(jq, st, n);
+    load_x(xb_, st, n, jq);
+    nj = nx;
+    if (colmap) {
+      n = nj.next_any(st);
+      load_j(jq, st, n);
+    }
   }
 
   int s = 0, par = 0, xpar = 0;
@@ -449,7 +473,11 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
       {
         int32_t st2;
         const int n2 = nx.next_any(st2);
-        load_x(xb_, st2, n2);
+        load_x(xb_, st2, n2, jq);
+        if (colmap) {
+          const int n3 = nj.next_any(st2);
+          load_j(jq, st2, n3);
+        }
       }
       const uint32_t xslot = xs_w + (uint32_t)(xpar * S * NB * 32) * 4u;
       xpar ^= 1;
@@ -487,6 +515,38 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
     const bool has_weak = g.k > 0 && u0 <= base + g.nsteps && u1 > base + g.nsteps;
     const bool last_piece = u1 >= base + n_rb;    // holds the row-block's last unit
     const bool whole = u0 <= base && last_piece;
+    if (has_weak) {
+      // fp16 weak columns x gathered fp16 activations, fp32: warp w folds
+      // chunks w, w + NW, ... (8 columns each) into its partial rows
+      const uint8_t* wb = p.blob + g.weak_off + rb * g.weak_rb_bytes;
+      const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
+      for (int ch = w; ch < g.kpad / kWeakChunk; ch += NW) {
+        uint4 a[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) a[r] = __ldg(reinterpret_cast<const uint4*>(wb + (int64_t)ch * kWeakChunkBytes) + 4 * lane + r);
+        const uint4 iv = __ldg(reinterpret_cast<const uint4*>(widx + ch * kWeakChunk));
+        const uint32_t iw[4] = {iv.x, iv.y, iv.z, iv.w};
+        float xw[8][NB];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int j = (int)((iw[c >> 1] >> (16 * (c & 1))) & 0xFFFFu);
+          const bool ok = ch * kWeakChunk + c < g.k;   // padding columns hold v = 0 and idx = 0
+#pragma unroll
+          for (int b = 0; b < NB; ++b) xw[c][b] = ok ? __half2float(p.x[(int64_t)b * p.xK + j]) : 0.f;
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t av[4] = {a[r].x, a[r].y, a[r].z, a[r].w};
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const __half2 h2 = *reinterpret_cast<const __half2*>(&av[c >> 1]);
+            const float wv = (c & 1) ? __high2float(h2) : __low2float(h2);
+#pragma unroll
+            for (int b = 0; b < NB; ++b) tot[b][r] = fmaf(wv, xw[c][b], tot[b][r]);
+          }
+        }
+      }
+    }
     float* rd = red + par * NW * NB * 128;
 #pragma unroll
     for (int b = 0; b < NB; ++b)
@@ -505,25 +565,6 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
 #pragma unroll
         for (int ww = 0; ww < NW; ++ww) a += rd[(ww * NB + b) * 128 + row];
         v[b] = a;
-      }
-      if (has_weak) {   // fp16 weak columns x gathered fp16 activations, fp32
-        const uint8_t* wb = p.blob + g.weak_off + rb * g.weak_rb_bytes;
-        const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
-        for (int ch = 0; ch < g.kpad / kWeakChunk; ++ch) {
-          const uint4 a = __ldg(reinterpret_cast<const uint4*>(wb + (int64_t)ch * kWeakChunkBytes) + row);
-          const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int t = ch * 8 + c;
-            if (t < g.k) {
-              const __half2 h2 = *reinterpret_cast<const __half2*>(&aw[c >> 1]);
-              const float wv = (c & 1) ? __high2float(h2) : __low2float(h2);
-              const int j = __ldg(widx + t);
-#pragma unroll
-              for (int b = 0; b < NB; ++b) v[b] = fmaf(wv, __half2float(p.x[(int64_t)b * p.xK + j]), v[b]);
-            }
-          }
-        }
       }
       const int64_t grow = rb * kRowBlock + row;
       if (whole) {
@@ -583,8 +624,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
 // Device inverse of layout 4 (test hook): one thread per (row, column).
 __global__ void owq_unpack_codes_cc_kernel(const uint8_t* blob, Geo g, uint8_t* codes) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (int64_t)g.M * g.K) return;
-  const int64_t row = i / g.K, col = i - row * g.K;
+  if (i >= (int64_t)g.M * g.Ks) return;
+  const int64_t row = i / g.Ks, col = i - row * g.Ks;
   const int64_t rb = row / kRowBlock, rr = row % kRowBlock, step = col / kStep, j = col % kStep;
   const uint8_t* it = blob + g.units_off + item_offset(g, rb, step);
   const int lane = (int)(rr >> 2), r = (int)(rr & 3);
@@ -658,7 +699,7 @@ owq_status gemm(const Geo& g, const void* blob, const uint16_t* x, int B, void* 
   struct SpanCache { int64_t key[3]; int32_t span[kMaxGrid + 1]; };
   static thread_local SpanCache cache[8];
   static thread_local int cache_n = 0, cache_next = 0;
-  const int64_t key[3] = {((int64_t)g.nrb << 32) | g.nsteps, ((int64_t)g.kpad << 32) | g.W, grid};
+  const int64_t key[3] = {((int64_t)g.nrb << 32) | g.nsteps, ((int64_t)g.kpad << 32) | g.W, grid};   // nsteps covers Ks
   static thread_local Params p;   // large (span table); filled per call
   int hit = -1;
   for (int i = 0; i < cache_n && hit < 0; ++i)
@@ -699,7 +740,7 @@ owq_status gemm(const Geo& g, const void* blob, const uint16_t* x, int B, void* 
 }
 
 owq_status unpack(const Geo& g, const void* blob, uint8_t* codes, cudaStream_t stream) {
-  const int64_t n = (int64_t)g.M * g.K;
+  const int64_t n = (int64_t)g.M * g.Ks;
   owq_unpack_codes_cc_kernel<<<(unsigned)((n + 255) / 256), 256, 0, stream>>>((const uint8_t*)blob, g, codes);
   return cudaGetLastError() == cudaSuccess ? OWQ_OK : OWQ_ERR_CUDA;
 }

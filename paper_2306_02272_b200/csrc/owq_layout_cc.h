@@ -29,7 +29,12 @@
 //   sz      [nrb][G][128] (scale, zero) fp16 pairs (row-block-major)
 //   weak    [nrb][kpad/8][128 rows][8] fp16 weak values (zero-padded to 8)
 //   widx    [kpad] u16 weak-column indices (zero-padded)
-//   wmask   [nsteps] u32, bit j of word s = column 32 s + j is weak
+//   wmask   [nsteps] u32, bit j of word s = stored column 32 s + j is weak
+//   colmap  [nsteps * 32] u16 (only when Ks-mapped): original column
+//           of each stored position (act-order / storage-favored variants,
+//           P:411-412); without it stored position = original column.
+// Ks = stored columns (K without a map); steps, groups and the weak mask run
+// over stored positions; x and the weak indices keep the original K columns.
 #pragma once
 #include <stdint.h>
 
@@ -56,17 +61,21 @@ OWQ_CC_HD int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 struct Geo {
   int32_t M, K, bits, group, k;
   int32_t nrb, nsteps, kpad, G, W;
+  int32_t Ks, mapped;         // stored columns; 1 = a column map is stored
   int64_t item_bytes, rb_code_bytes, weak_rb_bytes;
-  int64_t units_off, sz_off, weak_off, widx_off, wmask_off, total;
+  int64_t units_off, sz_off, weak_off, widx_off, wmask_off, colmap_off, total;
 };
 
-OWQ_CC_HD Geo make_geo(int32_t M, int32_t K, int32_t bits, int32_t group, int32_t k) {
+// Ks < 0: no column map (Ks = K).
+OWQ_CC_HD Geo make_geo(int32_t M, int32_t K, int32_t bits, int32_t group, int32_t k, int32_t Ks = -1) {
   Geo g{};
   g.M = M; g.K = K; g.bits = bits; g.group = group; g.k = k;
+  g.mapped = Ks >= 0 ? 1 : 0;
+  g.Ks = Ks >= 0 ? Ks : K;
   g.nrb = (int32_t)cdiv(M, kRowBlock);
-  g.nsteps = (int32_t)cdiv(K, kStep);
+  g.nsteps = (int32_t)cdiv(g.Ks, kStep);
   g.kpad = (int32_t)cdiv(k, kWeakChunk) * kWeakChunk;
-  g.G = group ? (int32_t)cdiv(K, group) : 1;
+  g.G = group ? (int32_t)cdiv(g.Ks, group) : 1;
   g.W = words_per_row(bits);
   g.item_bytes = (int64_t)g.W * 32 * 16;
   g.rb_code_bytes = (int64_t)g.nsteps * g.item_bytes;
@@ -76,7 +85,8 @@ OWQ_CC_HD Geo make_geo(int32_t M, int32_t K, int32_t bits, int32_t group, int32_
   g.weak_off = g.sz_off + (int64_t)g.nrb * g.G * kSZBlockBytes;
   g.widx_off = g.weak_off + (int64_t)g.nrb * g.weak_rb_bytes;
   g.wmask_off = g.widx_off + cdiv((int64_t)g.kpad * 2 + 2, 16) * 16;
-  g.total = g.wmask_off + cdiv((int64_t)g.nsteps * 4, 16) * 16;
+  g.colmap_off = g.wmask_off + cdiv((int64_t)g.nsteps * 4, 16) * 16;
+  g.total = g.colmap_off + (g.mapped ? cdiv((int64_t)g.nsteps * kStep * 2, 16) * 16 : 0);
   return g;
 }
 
@@ -134,6 +144,7 @@ struct BlobHeader {          // first bytes of the blob (version 4)
   int32_t M, K, bits, group, k;
   int32_t nrb, nsteps, kpad, G, W;
   int64_t total;
+  int32_t Ks, mapped;
 };
 constexpr uint32_t kMagic = 0x4257514Fu;     // same magic as version 3: the version field tells them apart
 

@@ -56,7 +56,9 @@ int n_groups(const owq_shape* s) { return s->group_size ? (s->c_in + s->group_si
 
 // Validated, decoded view of an owq_host_layer.
 struct Layer {
-  int M, K, bits, group, k, G;
+  int M, K, bits, group, k, G;     // K = stored columns (= c_in without a column map)
+  int Korig = 0;                   // c_in (x width) when a column map is present
+  std::vector<uint16_t> colmap;    // stored position -> original column (empty: identity)
   std::vector<uint8_t> codes;      // [M][K], weak columns already zero-filled
   const uint16_t* scale;
   const uint16_t* zero;
@@ -187,12 +189,14 @@ void write_blob(const Layer& L, uint8_t* blob) {
 // subnormal (bit offset p(j) + bits <= 24 inside the register it is read from).
 void write_blob_cc(const Layer& L, uint8_t* blob) {
   namespace C = owq::cc;
-  const C::Geo g = C::make_geo(L.M, L.K, L.bits, L.group, L.k);
+  const bool mapped = !L.colmap.empty() || L.Korig > 0;
+  const C::Geo g = mapped ? C::make_geo(L.M, L.Korig, L.bits, L.group, L.k, L.K) : C::make_geo(L.M, L.K, L.bits, L.group, L.k);
   std::memset(blob, 0, (size_t)g.total);
   C::BlobHeader h{};
   h.magic = C::kMagic; h.version = C::kVersion;
-  h.M = L.M; h.K = L.K; h.bits = L.bits; h.group = L.group; h.k = L.k;
+  h.M = L.M; h.K = g.K; h.bits = L.bits; h.group = L.group; h.k = L.k;
   h.nrb = g.nrb; h.nsteps = g.nsteps; h.kpad = g.kpad; h.G = g.G; h.W = g.W; h.total = g.total;
+  h.Ks = g.Ks; h.mapped = g.mapped;
   std::memcpy(blob, &h, sizeof(h));
 #pragma omp parallel for schedule(dynamic, 1)
   for (int rb = 0; rb < g.nrb; ++rb) {
@@ -234,10 +238,68 @@ void write_blob_cc(const Layer& L, uint8_t* blob) {
       }
   }
   uint32_t* mask = reinterpret_cast<uint32_t*>(blob + g.wmask_off);
-  for (int t = 0; t < L.k; ++t) {
-    std::memcpy(blob + g.widx_off + 2 * t, &L.widx[t], 2);
-    mask[L.widx[t] >> 5] |= 1u << (L.widx[t] & 31);
+  for (int t = 0; t < L.k; ++t) std::memcpy(blob + g.widx_off + 2 * t, &L.widx[t], 2);
+  if (mapped) {
+    // weak mask over stored positions; the column map itself
+    std::vector<char> is_weak((size_t)g.K, 0);
+    for (int t = 0; t < L.k; ++t) is_weak[L.widx[t]] = 1;
+    uint16_t* cm = reinterpret_cast<uint16_t*>(blob + g.colmap_off);
+    for (int p = 0; p < g.Ks; ++p) {
+      cm[p] = L.colmap[p];
+      if (is_weak[L.colmap[p]]) mask[p >> 5] |= 1u << (p & 31);
+    }
+  } else {
+    for (int t = 0; t < L.k; ++t) mask[L.widx[t] >> 5] |= 1u << (L.widx[t] & 31);
   }
+}
+
+// Layer with a column map (NEXT-4: act-order / storage-favored, layout 4 only):
+// codes [M][Ks] and scale/zero [M][ceil(Ks/g)] in stored order; weak indices
+// and values in original columns; stored positions of weak columns zero-filled.
+owq_status load_layer_map(const owq_shape* s, const owq_host_layer* L, const owq_colmap* map, int flags, Layer& out) {
+  owq_status st = check_shape(s);
+  if (st != OWQ_OK) return st;
+  if (!map || !map->colmap || map->k_stored <= 0 || map->k_stored > s->c_in) return OWQ_ERR_INVALID_ARG;
+  if (!L || !L->codes || !L->scale || !L->zero) return OWQ_ERR_INVALID_ARG;
+  if (s->n_weak > 0 && (!L->weak_idx || !L->weak_val)) return OWQ_ERR_INVALID_ARG;
+  const int K = s->c_in, Ks = map->k_stored, k = s->n_weak;
+  std::vector<char> seen((size_t)K, 0);
+  for (int p = 0; p < Ks; ++p) {
+    const int c = map->colmap[p];
+    if (c >= K || seen[c]) return OWQ_ERR_INVALID_ARG;   // in range and injective
+    seen[c] = 1;
+  }
+  for (int t = 0; t < k; ++t) {
+    if (L->weak_idx[t] >= K) return OWQ_ERR_WEAK_INDEX;
+    if (t && L->weak_idx[t] <= L->weak_idx[t - 1]) return OWQ_ERR_WEAK_INDEX;
+  }
+  // codes / grids over the stored positions, validated without the weak handling
+  owq_shape ss = *s;
+  ss.c_in = Ks;
+  ss.n_weak = 0;
+  owq_host_layer ls = *L;
+  ls.weak_idx = nullptr;
+  ls.weak_val = nullptr;
+  st = load_layer(&ss, &ls, flags & ~OWQ_PACK_STRICT, out);
+  if (st != OWQ_OK) return st;
+  out.k = k; out.widx = L->weak_idx; out.wval = L->weak_val;
+  out.Korig = K;
+  out.colmap.assign(map->colmap, map->colmap + Ks);
+  std::vector<char> is_weak((size_t)K, 0);
+  for (int t = 0; t < k; ++t) is_weak[L->weak_idx[t]] = 1;
+  int fill_err = 0;
+  for (int i = 0; i < out.M; ++i)
+    for (int p = 0; p < Ks; ++p)
+      if (is_weak[out.colmap[p]]) {
+        const int gi = out.group ? p / out.group : 0;
+        const uint8_t z = (uint8_t)half_to_float(out.zero[(size_t)i * out.G + gi]);
+        uint8_t& c = out.codes[(size_t)i * Ks + p];
+        if (c != z) {
+          if (flags & OWQ_PACK_STRICT) fill_err = 1;
+          c = z;
+        }
+      }
+  return fill_err ? OWQ_ERR_ZERO_FILL : OWQ_OK;
 }
 
 owq_status decode_cc(const void* h_blob, size_t bytes, owq_shape* shape_out, uint8_t* codes, uint16_t* scale,
@@ -247,14 +309,14 @@ owq_status decode_cc(const void* h_blob, size_t bytes, owq_shape* shape_out, uin
   std::memcpy(&h, h_blob, sizeof(h));
   owq_shape s{h.M, h.K, h.bits, h.group, h.k};
   if (!shape_ok(&s)) return OWQ_ERR_BAD_BLOB;
-  const C::Geo g = C::make_geo(h.M, h.K, h.bits, h.group, h.k);
+  const C::Geo g = h.mapped ? C::make_geo(h.M, h.K, h.bits, h.group, h.k, h.Ks) : C::make_geo(h.M, h.K, h.bits, h.group, h.k);
   if ((size_t)g.total > bytes || g.total != h.total) return OWQ_ERR_BAD_BLOB;
   const uint8_t* blob = (const uint8_t*)h_blob;
   if (shape_out) *shape_out = s;
   for (int row = 0; row < h.M; ++row) {
     const int rb = row / C::kRowBlock, rr = row % C::kRowBlock, lane = rr >> 2, r = rr & 3;
     if (codes)
-      for (int col = 0; col < h.K; ++col) {
+      for (int col = 0; col < g.Ks; ++col) {
         const uint8_t* it = blob + g.units_off + C::item_offset(g, rb, col / C::kStep);
         uint32_t c = 0;
         for (int bit = 0; bit < h.bits; ++bit) {
@@ -264,7 +326,7 @@ owq_status decode_cc(const void* h_blob, size_t bytes, owq_shape* shape_out, uin
           std::memcpy(&v, it + (word * 32 + lane) * 16 + r * 4, 4);
           c |= ((v >> pos) & 1u) << bit;
         }
-        codes[(size_t)row * h.K + col] = (uint8_t)c;
+        codes[(size_t)row * g.Ks + col] = (uint8_t)c;
       }
     for (int gi = 0; gi < g.G; ++gi) {
       uint16_t pair[2];
@@ -392,6 +454,40 @@ owq_status owq_pack_host(const owq_shape* s, const owq_host_layer* L, int flags,
   if (blob_bytes < owq_packed_bytes_layout(s, cc ? OWQ_LAYOUT_CC : OWQ_LAYOUT_VERSION)) return OWQ_ERR_BUFFER_TOO_SMALL;
   if (cc) write_blob_cc(lay, (uint8_t*)h_blob);
   else write_blob(lay, (uint8_t*)h_blob);
+  return OWQ_OK;
+}
+
+size_t owq_packed_bytes_colmap(const owq_shape* s, const owq_colmap* map) {
+  if (!shape_ok(s) || !map || map->k_stored <= 0 || map->k_stored > s->c_in) return 0;
+  return (size_t)owq::cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak, map->k_stored).total;
+}
+
+owq_status owq_pack_host_colmap(const owq_shape* s, const owq_host_layer* L, const owq_colmap* map, int flags,
+                                void* h_blob, size_t blob_bytes) {
+  if (!h_blob) return OWQ_ERR_INVALID_ARG;
+  Layer lay;
+  owq_status st = load_layer_map(s, L, map, flags, lay);
+  if (st != OWQ_OK) return st;
+  if (blob_bytes < owq_packed_bytes_colmap(s, map)) return OWQ_ERR_BUFFER_TOO_SMALL;
+  write_blob_cc(lay, (uint8_t*)h_blob);
+  return OWQ_OK;
+}
+
+owq_status owq_blob_colmap_host(const void* h_blob, size_t bytes, int32_t* k_stored, uint16_t* colmap) {
+  namespace C = owq::cc;
+  if (!h_blob || bytes < (size_t)C::kHeaderBytes) return OWQ_ERR_INVALID_ARG;
+  C::BlobHeader h;
+  std::memcpy(&h, h_blob, sizeof(h));
+  if (h.magic != C::kMagic || h.version != (uint32_t)OWQ_LAYOUT_CC) return OWQ_ERR_BAD_BLOB;
+  const C::Geo g = h.mapped ? C::make_geo(h.M, h.K, h.bits, h.group, h.k, h.Ks) : C::make_geo(h.M, h.K, h.bits, h.group, h.k);
+  if ((size_t)g.total > bytes) return OWQ_ERR_BAD_BLOB;
+  if (k_stored) *k_stored = g.Ks;
+  if (colmap)
+    for (int p = 0; p < g.Ks; ++p) {
+      uint16_t v = (uint16_t)p;
+      if (h.mapped) std::memcpy(&v, (const uint8_t*)h_blob + g.colmap_off + 2 * p, 2);
+      colmap[p] = v;
+    }
   return OWQ_OK;
 }
 

@@ -150,3 +150,51 @@ def test_cc_strict_and_errors():
         owq.owq_pack_host(shape, d, flags=owq.OWQ_PACK_LAYOUT_CC | owq.OWQ_PACK_STRICT)
     assert owq.owq_packed_bytes_layout(shape, 5) == 0
     assert owq.owq_packed_bytes_layout(owq.Shape(64, 128, 5, 0, 2), owq.OWQ_LAYOUT_CC) == 0
+
+
+# ---------------------------------------------------------------- NEXT-4: column-mapped blobs
+@pytest.mark.parametrize("mode,group", [("latency", 0), ("storage", 0), ("latency", 128), ("storage", 128)])
+def test_colmap_round_trip(mode, group):
+    from owq_testutil import dict_from_stored, synthetic_stored
+    rep = synthetic_stored(200, 700, 4 if group else 3, group, 9, mode, seed=5)
+    d = dict_from_stored(rep)
+    shape = owq.Shape(200, 700, rep.bits, group, 9)
+    blob = owq.owq_pack_host_colmap(shape, d, d["colmap"], flags=owq.OWQ_PACK_U8_CODES)
+    assert blob.size == owq.owq_packed_bytes_colmap(shape, d["colmap"])
+    assert np.array_equal(owq.owq_blob_colmap_host(blob), d["colmap"])
+    out = owq.owq_blob_decode_host(blob)
+    assert out["codes"].shape == (200, rep.Ks)
+    assert np.array_equal(out["codes"], d["codes"])
+    assert np.array_equal(out["scale_f16"], d["scale_f16"]) and np.array_equal(out["zero_f16"], d["zero_f16"])
+    assert np.array_equal(out["weak_val_f16"], d["weak_val_f16"])
+    # weak mask over stored positions
+    g = geo(200, rep.Ks, rep.bits, group, 9)
+    hdr = blob[:256]
+    wmask_off = g["wmask"]
+    wm = blob[wmask_off:wmask_off + 4 * g["nsteps"]].view(np.uint32)
+    ws = set(int(j) for j in rep.weak_idx)
+    for p in range(rep.Ks):
+        assert bool((wm[p >> 5] >> (p & 31)) & 1) == (int(rep.colmap[p]) in ws)
+
+
+def test_colmap_validation():
+    from owq_testutil import dict_from_stored, synthetic_stored
+    rep = synthetic_stored(64, 100, 3, 0, 4, "storage", seed=1)
+    d = dict_from_stored(rep)
+    shape = owq.Shape(64, 100, 3, 0, 4)
+    bad = d["colmap"].copy()
+    bad[1] = bad[0]                                     # repeated column
+    with pytest.raises(owq.OwqError, match="INVALID_ARG"):
+        owq.owq_pack_host_colmap(shape, d, bad, flags=owq.OWQ_PACK_U8_CODES)
+    bad = d["colmap"].copy()
+    bad[0] = 100                                        # out of range
+    with pytest.raises(owq.OwqError, match="INVALID_ARG"):
+        owq.owq_pack_host_colmap(shape, d, bad, flags=owq.OWQ_PACK_U8_CODES)
+    # latency-favored with a weak stored position not zero-filled: strict rejects
+    lat = synthetic_stored(64, 100, 3, 0, 4, "latency", seed=2)
+    dl = dict_from_stored(lat)
+    dl["codes"] = dl["codes"].copy()
+    dl["codes"][:, -1] = (dl["codes"][:, -1] + 1) % 8
+    with pytest.raises(owq.OwqError, match="ZERO_FILL"):
+        owq.owq_pack_host_colmap(owq.Shape(64, 100, 3, 0, 4), dl, dl["colmap"],
+                                 flags=owq.OWQ_PACK_U8_CODES | owq.OWQ_PACK_STRICT)
