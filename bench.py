@@ -138,12 +138,16 @@ def oracle_sample(layers_host, rows_per_layer):
 
 
 def host_sample(rows, batch):
-    """Seeded sample rows of the workload for the CPU oracle (same generators)."""
+    """Seeded sample rows of the workload for the CPU oracle (same generators;
+    q, k and v share one input, as in the GPU arm)."""
     import synth
     out = []
     for i, (name, M, K, k) in enumerate(LAYERS):
         d = synth.representation(rows, K, BITS, 0, k, seed=synth.SEED_BASE + 100 * i)
-        d["x"] = synth.activations(batch, K, seed=synth.SEED_BASE + 100 * i + 1, outliers=d["weak_idx"][:8])
+        if name in ("k", "v"):
+            d["x"] = out[0]["x"]
+        else:
+            d["x"] = synth.activations(batch, K, seed=synth.SEED_BASE + 100 * i + 1, outliers=d["weak_idx"][:8])
         out.append(d)
     return out
 
@@ -193,15 +197,34 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
-def build_layers(dev, batch, world, rank, keep_rows):
+# BASELINE configs measured beside the headline (per-layer device time, the
+# layout choose_layout() picks; parity-test shapes, reported, not the headline)
+SECONDARY = {
+    "opt6.7b_3.01bit_b1": [("qkvo", 4096, 4096, 3, 0, 5, 1), ("fc1", 16384, 4096, 3, 0, 1, 1),
+                           ("fc2", 4096, 16384, 3, 0, 5, 1)],
+    "llama7b_4bit_g128": [(f"{n}_b{B}", M, K, 4, 128, k, B) for B in (1, 4, 8, 16)
+                          for n, M, K, k in (("qkvo", 4096, 4096, 4), ("up", 11008, 4096, 1), ("down", 4096, 11008, 4))],
+    "opt66b_3.01bit_b1": [("qkvo", 9216, 9216, 3, 0, 11, 1), ("fc1", 36864, 9216, 3, 0, 2, 1),
+                          ("fc2", 9216, 36864, 3, 0, 11, 1)],
+}
+
+
+def build_layers(dev, batch, world, rank, keep_rows, layout_override=None):
     import torch
 
     import paper_2306_02272_b200 as owq
     import synth
     layers, host_keep = [], []
+    x_shared = None
     for i, (name, M, K, k) in enumerate(LAYERS):
         d = synth.representation(M, K, BITS, 0, k, seed=synth.SEED_BASE + 100 * i)
-        x = synth.activations(batch, K, seed=synth.SEED_BASE + 100 * i + 1, outliers=d["weak_idx"][:8])
+        # q, k and v read the SAME activation (the model's structure); out, fc1, fc2 their own
+        if name in ("q", "k", "v") and x_shared is not None:
+            x = x_shared
+        else:
+            x = synth.activations(batch, K, seed=synth.SEED_BASE + 100 * i + 1, outliers=d["weak_idx"][:8])
+        if name == "q":
+            x_shared = x
         if keep_rows:
             host_keep.append({"codes": d["codes"][:keep_rows].copy(), "scale_f16": d["scale_f16"][:keep_rows].copy(),
                               "zero_f16": d["zero_f16"][:keep_rows].copy(), "weak_idx": d["weak_idx"].copy(),
@@ -210,8 +233,13 @@ def build_layers(dev, batch, world, rank, keep_rows):
         L = {"name": name, "M": M, "K": K, "k": k, "full": full}
         if world == 1:
             L["shape"] = full
-            L["packed"] = owq.owq_pack(full, d, device=dev)
-            L["x"] = torch.from_numpy(x).to(dev)
+            L["layout"] = layout_override or owq.choose_layout(full, batch)
+            flags = owq.OWQ_PACK_LAYOUT_CC if L["layout"] == owq.OWQ_LAYOUT_CC else 0
+            L["packed"] = owq.owq_pack(full, d, flags=flags, device=dev)
+            if name in ("k", "v"):
+                L["x"] = layers[0]["x"]          # the same device tensor as q's input
+            else:
+                L["x"] = torch.from_numpy(x).to(dev)
             L["y"] = torch.empty((batch, M), dtype=torch.float16, device=dev)
             L["ws"] = owq.workspace(full, batch, dev)
             L["bytes"] = algorithmic_bytes(M, K, k, batch)
@@ -219,7 +247,7 @@ def build_layers(dev, batch, world, rank, keep_rows):
             mode = TP_MODE[name]
             ss, packed = owq.owq_tp_shard(full, d, mode, world, rank, device=dev)
             a, b = owq.owq_tp_bounds(full, mode, world, rank)
-            L.update(mode=mode, shape=ss, packed=packed, a=a, b=b)
+            L.update(mode=mode, shape=ss, packed=packed, a=a, b=b, layout=owq.OWQ_LAYOUT_TC)
             if mode == 0:
                 L["x"] = torch.from_numpy(x).to(dev)
                 L["y"] = torch.empty((batch, ss.c_out), dtype=torch.float16, device=dev)
@@ -260,6 +288,85 @@ def launch(L, tp=None, stream=None):
         owq.owq_tp_gemv(tp, L["mode"], L["full"], L["shape"], L["packed"], L["x"], L["y"], ws=L["ws"])
 
 
+def launches_per_call(L, world):
+    """Our kernels per public call: tcgen05 layout = x-digit pass + GEMV; CUDA-core
+    layout = one GEMV per 4 batch rows; + the fp32 -> fp16 convert of a
+    column-split layer's all-reduced y under TP."""
+    import paper_2306_02272_b200 as owq
+    B = L["x"].shape[0]
+    n = 2 if L.get("layout", owq.OWQ_LAYOUT_TC) == owq.OWQ_LAYOUT_TC else -(-B // 4)
+    return n + (1 if world > 1 and L.get("mode", 0) == 1 else 0)
+
+
+def time_graph_calls(seq, stream, tp=None, reps=2):
+    """Device time of the calls in `seq`, captured back to back in one CUDA graph
+    (events on the launching stream; the first replay warms up)."""
+    import torch
+    pg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(pg, stream=stream):
+        for L in seq:
+            launch(L, tp)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            e0.record(stream)
+            pg.replay()
+            e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def measure_secondary(dev, stream, budget_s):
+    """Per-layer device time of the SECONDARY configs (rotating packed copies >
+    3x L2, back-to-back calls in one graph)."""
+    import torch
+
+    import paper_2306_02272_b200 as owq
+    import synth
+    out, t0 = {}, time.perf_counter()
+    for cfg, rows in SECONDARY.items():
+        res = {}
+        for name, M, K, bits, group, k, B in rows:
+            if time.perf_counter() - t0 > budget_s:
+                res[name] = "skipped (time budget)"
+                continue
+            d = synth.representation(M, K, bits, group, k, seed=M + K + k)
+            shape = owq.Shape(M, K, bits, group, k)
+            lay = owq.choose_layout(shape, B)
+            flags = owq.OWQ_PACK_LAYOUT_CC if lay == owq.OWQ_LAYOUT_CC else 0
+            nb = owq.owq_packed_bytes_layout(shape, lay)
+            ncop = max(1, min(8, -(-400_000_000 // nb)))
+            packs = [owq.owq_pack(shape, d, flags=flags, device=dev) for _ in range(ncop)]
+            x = torch.from_numpy(synth.activations(B, K, seed=1, outliers=d["weak_idx"])).to(dev)
+            y = torch.empty((B, M), dtype=torch.float16, device=dev)
+            ws = owq.workspace(shape, B, dev)
+            R = 24
+            seq = [{"shape": shape, "packed": packs[i % ncop], "x": x, "y": y, "ws": ws} for i in range(R)]
+            with torch.cuda.stream(stream):
+                for L in seq[:ncop]:
+                    launch(L)
+            ms = time_graph_calls(seq, stream) / R
+            alg = algorithmic_bytes(M, K, k, B, bits=bits, G=(1 if group == 0 else -(-K // group)))
+            res[name] = {"us": round(ms * 1e3, 2), "GBps": round(alg / (ms * 1e-3) / 1e9, 1),
+                         "layout": "cc" if lay == owq.OWQ_LAYOUT_CC else "tc"}
+            del packs
+        out[cfg] = res
+    return out
+
+
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["model"] = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    return info
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -280,7 +387,8 @@ def run_gpu(args):
         dist.barrier()
     owq.lib()
     keep = args.ref_rows if (rank == 0 and not args.no_cpu) else 0
-    layers, host_keep = build_layers(dev, args.batch, world, rank, keep)
+    layout_override = {"tc": owq.OWQ_LAYOUT_TC, "cc": owq.OWQ_LAYOUT_CC}.get(args.layout)
+    layers, host_keep = build_layers(dev, args.batch, world, rank, keep, layout_override)
     tp = None
     if world > 1:
         uid = owq.owq_tp_get_unique_id() if rank == 0 else bytes(128)
@@ -289,7 +397,7 @@ def run_gpu(args):
         tp = owq.owq_tp_init(obj[0], world, rank)
     step_bytes = sum(L["bytes"] for L in layers)
     stream = torch.cuda.Stream(device=dev)
-    # q, k, v are independent (one input, three weights): on one GPU they run
+    # q, k, v read one input and are independent of each other: on one GPU they run
     # concurrently on three streams with a third of the SMs each, so their fixed
     # per-call costs (prologue, pipeline fill/drain, digit pass) overlap; out,
     # fc1, fc2 depend on their predecessors and run in order on all SMs.
@@ -325,14 +433,17 @@ def run_gpu(args):
         for _ in range(2):
             step()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
 
     K, W = args.steps, args.warmup
     n_l = len(layers)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    graph_ok = world == 1 and not args.no_graph
-    g = None
-    if graph_ok:
+    g = wg = sg = None
+    if not args.no_graph:
+        # K steps (and the warm-up) captured in CUDA graphs -- also under TP: the
+        # NCCL collectives of owq_tp_gemv are graph-capturable
         try:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
@@ -342,11 +453,16 @@ def run_gpu(args):
             with torch.cuda.graph(wg, stream=stream):
                 for _ in range(max(W, 3)):
                     step()
+            sg = torch.cuda.CUDAGraph()     # one step (per-step distribution, outside the timed region)
+            with torch.cuda.graph(sg, stream=stream):
+                step()
         except Exception as e:  # pragma: no cover - fall back to eager timing
             print(f"[bench] graph capture failed ({e}); timing eager launches", file=sys.stderr)
-            g = None
+            g = wg = sg = None
     uploaded = g is not None and graph_upload(g, stream) and graph_upload(wg, stream)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
 
     with ClockSampler(local) as clk:
         # warm-up (untimed)
@@ -378,10 +494,27 @@ def run_gpu(args):
         t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
+    ms_step = ms_total / K
+    value = step_bytes / (ms_step * 1e-3) / 1e9
+
+    # per-step distribution (outside the timed region): K single-step replays
+    step_ms = []
+    if sg is not None:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(min(K, 100))]
+        with torch.cuda.stream(stream):
+            for a_, b_ in evs:
+                a_.record(stream)
+                sg.replay()
+                b_.record(stream)
+        torch.cuda.synchronize()
+        step_ms = sorted(a_.elapsed_time(b_) for a_, b_ in evs)
+    pct = (lambda q: round(step_ms[min(len(step_ms) - 1, int(q * len(step_ms)))], 5)) if step_ms else (lambda q: None)
+
     # per-launch durations (roofline): per layer shape, R back-to-back calls in one
     # graph over the same-shape layers in rotation (working set > L2), CUDA events
-    # around the replay on the launching stream
+    # around the replay on the launching stream; + one call after an L2 flush
     per_layer_ms = [None] * n_l
+    single_ms = {}
     shapes = {}
     for i, L in enumerate(layers):
         shapes.setdefault((L["M"], L["K"]), []).append(i)
@@ -393,60 +526,72 @@ def run_gpu(args):
         if "ws_seq" in L:
             Lv["ws"] = L["ws_seq"]
         seq_view.append(Lv)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for idx in shapes.values():
         pool = [seq_view[i] for i in idx]
         nbytes = sum(L["bytes"] for L in pool)
-        # rotate over >= 3x L2 of distinct weights so every call streams from HBM:
-        # extra packed copies for shapes that occur once per step (fc1, fc2)
         while nbytes < 3 * 126e6 and world == 1:
             L0 = pool[len(pool) % len(idx)]
             Lc = dict(L0)
             Lc["packed"] = L0["packed"].clone()
             pool.append(Lc)
             nbytes += L0["bytes"]
+        with torch.cuda.stream(stream):
+            for L in pool:
+                launch(L, tp)
         seq = [pool[j % len(pool)] for j in range(R)]
-        if graph_ok:
-            pg = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(pg, stream=stream):
+        if g is not None:
+            ms = time_graph_calls(seq, stream, tp) / R
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
                 for L in seq:
                     launch(L, tp)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / R
+        for i in idx:
+            per_layer_ms[i] = ms
+        # single-launch latency: one call with a cold L2 (256 MB written first)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
-            for rep_ in range(2):   # first replay warms up
-                e0.record(stream)
-                if graph_ok:
-                    pg.replay()
-                else:
-                    for L in seq:
-                        launch(L, tp)
-                e1.record(stream)
+            flush.fill_(1)
+            e0.record(stream)
+            launch(pool[0], tp)
+            e1.record(stream)
         torch.cuda.synchronize()
-        for i in idx:
-            per_layer_ms[i] = e0.elapsed_time(e1) / R
-    ms_step = ms_total / K
-    value = step_bytes / (ms_step * 1e-3) / 1e9
+        single_ms[layers[idx[0]]["name"]] = e0.elapsed_time(e1)
+    del flush
 
     # ---------------------------------------------------------------- e2e (host buffers)
     e2e = None
     if not args.no_e2e:
-        # The step's inputs (every layer's x) sit in one pinned host buffer and go
-        # to the device in one copy; the step's results (every layer's y) come back
-        # in one copy; in between, the layers are eager public-API calls, one
-        # after another on all SMs (the three-stream q/k/v schedule costs more
-        # host time than it saves when not captured in a graph).
+        # The step's inputs (q's x -- shared by k and v -- and the x of out, fc1,
+        # fc2) sit in one pinned host buffer and go to the device in one copy;
+        # the step's results (every layer's y) come back in one copy; in between,
+        # the layers are eager public-API calls, one after another on all SMs.
         eager = [dict(L) for L in (seq_view if world == 1 else layers)]
-        nx = [L["x"].numel() for L in eager]
+        xs_unique = []
+        for L in eager:
+            if not any(L["x"] is u for u in xs_unique):
+                xs_unique.append(L["x"])
+        nx = [u.numel() for u in xs_unique]
         ny = [L["y"].numel() for L in eager]
         xh_all = torch.empty(sum(nx), dtype=torch.float16).pin_memory()
         yh_all = torch.empty(sum(ny), dtype=torch.float16).pin_memory()
         xd_all = torch.empty(sum(nx), dtype=torch.float16, device=dev)
         yd_all = torch.empty(sum(ny), dtype=torch.float16, device=dev)
-        ox = oy = 0
-        for L, a, b in zip(eager, nx, ny):
-            xh_all[ox:ox + a].copy_(L["x"].reshape(-1).cpu())
-            L["x"] = xd_all[ox:ox + a].view(L["x"].shape)
-            L["y"] = yd_all[oy:oy + b].view(L["y"].shape)
+        ox = 0
+        views = {}
+        for u, a in zip(xs_unique, nx):
+            xh_all[ox:ox + a].copy_(u.reshape(-1).cpu())
+            views[id(u)] = xd_all[ox:ox + a].view(u.shape)
             ox += a
+        oy = 0
+        for L, b in zip(eager, ny):
+            L["x"] = views[id(L["x"])]
+            L["y"] = yd_all[oy:oy + b].view(L["y"].shape)
             oy += b
         h2d = xh_all.numel() * 2
         d2h = yh_all.numel() * 2
@@ -474,7 +619,13 @@ def run_gpu(args):
             dt = float(t.item())
         e2e = {"value": round(step_bytes * E / dt / 1e9, 2), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": round(1e3 * dt / E, 4), "path": "one pinned H2D copy of every layer's x, eager public-API calls (all SMs, in order), one D2H copy of every y"}
+               "ms_per_step": round(1e3 * dt / E, 4),
+               "path": "one pinned H2D copy of the step's inputs (q/k/v share one x), eager public-API calls "
+                       "(all SMs, in order), one D2H copy of every y"}
+
+    secondary = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        secondary = measure_secondary(dev, stream, args.secondary_seconds)
 
     if rank != 0:
         if world > 1:
@@ -485,61 +636,99 @@ def run_gpu(args):
     # ---------------------------------------------------------------- roofline / cpu baseline
     peaks = measured_peaks()
     peak = peaks.get("hbm_gbs")
+    read_peak = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "read_peak.json")) as f:
+            read_peak = json.load(f).get("read_only_gbs_tma_1GiB")
+    except Exception:
+        pass
     per_layer = {L["name"]: {"us": round(1e3 * t, 3), "GBps": round(L["bytes"] / (t * 1e-3) / 1e9, 1),
-                             "bytes": int(L["bytes"])} for L, t in zip(layers, per_layer_ms)}
+                             "bytes": int(L["bytes"]), "single_launch_us_cold_l2": (round(1e3 * single_ms[L["name"]], 2) if L["name"] in single_ms else None),
+                             "layout": "cc" if L.get("layout") == owq.OWQ_LAYOUT_CC else "tc"}
+                 for L, t in zip(layers, per_layer_ms)}
     kern_ms = sum(per_layer_ms)
     achieved = step_bytes / (kern_ms * 1e-3) / 1e9 if world == 1 else value
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f)
-        traffic = tr.get("bytes_per_step") and tr["bytes_per_step"] / len(layers)
+            tr = json.load(f)["per_shape"]
+        tag = {(D, D): "q", (4 * D, D): "fc1", (D, 4 * D): "fc2"}
+        per = [tr[tag[(L["M"], L["K"])]] for L in layers]
+        traffic = round(sum(t["dram_read_bytes"] + t["dram_write_bytes"] for t in per) / len(per), 1)
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4) if peak else None, "traffic": traffic,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, measured)" if peak else "missing",
+                "read_only_peak": read_peak,
+                "frac_of_read_only_peak": round(achieved / read_peak, 4) if read_peak else None,
                 "frac_of_nominal_8TBps": round(achieved / NOMINAL_HBM_GBS, 4),
                 "per_launch": "per layer shape: R back-to-back calls in one CUDA graph timed with CUDA events; "
-                              "a call = the x-digit pass + the fused GEMV (both counted, so achieved is conservative)"}
+                              "achieved = sum of the layers' algorithmic bytes / sum of their per-call times "
+                              "(a tcgen05-layout call = x-digit pass + GEMV, both counted)",
+                "traffic_note": "mean per launch of dram__bytes_read.sum + dram__bytes_write.sum from "
+                                "profiles/ncu_traffic.json (one --set full capture per layer shape)"}
     cpu = None
     if not args.no_cpu and host_keep:
         lim = cpu_threads()
-        ctx = lim(limits=1) if lim else None
-        if ctx:
-            ctx.__enter__()
-        # repeat the sample until about args.cpu_seconds of CPU work (bounded: at most 64 passes)
-        t, nb, passes = 0.0, 0.0, 0
-        while passes < 64 and (passes == 0 or t < args.cpu_seconds):
-            dt, dnb = oracle_sample(host_keep, args.ref_rows)
-            t, nb, passes = t + dt, nb + dnb, passes + 1
-        if ctx:
-            ctx.__exit__(None, None, None)
-        cpu = {"value": round(nb / t / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+        runs = []
+        for threads in (1, None):
+            ctx = lim(limits=threads) if lim else None
+            if ctx:
+                ctx.__enter__()
+            # repeat the sample until about args.cpu_seconds of CPU work (bounded: at most 64 passes)
+            t, nb, passes = 0.0, 0.0, 0
+            while passes < 64 and (passes == 0 or t < args.cpu_seconds / 2):
+                dt, dnb = oracle_sample(host_keep, args.ref_rows)
+                t, nb, passes = t + dt, nb + dnb, passes + 1
+            if ctx:
+                ctx.__exit__(None, None, None)
+            runs.append((threads or os.cpu_count(), nb / t / 1e9, passes, t))
+        best = max(runs, key=lambda r: r[1])
+        hi = host_info()
+        cpu = {"value": round(best[1], 4), "unit": UNIT, "cores": best[0], "kind": "oracle",
                "sample": f"oracle.matvec_rows (fp64) on the first {args.ref_rows} rows of each of the 6 layers, "
-                         f"{passes} passes, 1 thread",
-               "seconds": round(t, 3)}
+                         f"{best[2]} passes, {best[0]} thread(s) (BLAS threads via threadpoolctl)",
+               "seconds": round(best[3], 3),
+               "runs": [{"threads": r[0], "GBps": round(r[1], 4), "passes": r[2], "seconds": round(r[3], 3)} for r in runs],
+               "host": hi}
+        if args.quantizer_time:
+            import oracle as O
+            import synth
+            Wq, Xq, _ = synth.weights_and_calib(768, 768, N=2048, n_outliers=8, seed=2306)
+            t0 = time.perf_counter()
+            O.owq_quantize(Wq, Xq, 3, 8)
+            cpu["oracle_quantizer_config1_s"] = round(time.perf_counter() - t0, 2)
+    lays = {L.get("layout") for L in layers}
+    arith = []
+    if owq.OWQ_LAYOUT_TC in lays:
+        arith.append("tcgen05 layout: codes (u8) x exact int8 digits of x*2^24 on tcgen05.mma kind::i8, s32 accumulate; "
+                     "zero point and digits combined exactly (fp64), fp32 scale")
+    if owq.OWQ_LAYOUT_CC in lays:
+        arith.append("CUDA-core layout: exact products q*x (fp32 subnormal codes x 2^(111-p)-scaled x, FFMA2), fp32 sums, "
+                     "factored zero point s*(sum q x - z sum x)")
+    arith.append("weak columns fp16 x fp16 in fp32")
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": W, "ms_per_step": round(ms_step, 5), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u8*s8->s32", "data": "synthetic",
+        "vs_baseline": None, "dtype": "u8*s8->s32" if lays == {owq.OWQ_LAYOUT_TC} else "mixed (see config.arith)",
+        "data": "synthetic",
         "config": {"workload": WORKLOAD, "layers": [[n, M, K_, k] for n, M, K_, k in LAYERS],
                    "bits": BITS, "group_size": 0, "batch": args.batch,
                    "parallelism": f"tp{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (682 MB of packed weights per step vs 126 MB L2); no flush",
                    "graph": g is not None, "graph_uploaded_before_timing": bool(uploaded) if g is not None else None,
-                   "schedule": ("q, k, v concurrently on 3 streams (a third of the SMs each); out, fc1, fc2 in order"
-                                if concurrent else "all six layers in order on all SMs"),
-                   "arith": "codes (u8) x exact int8 digits of x*2^24 on tcgen05.mma kind::i8, s32 accumulate; "
-                            "zero point and digits combined exactly (fp64), fp32 scale; weak columns fp16 x fp16, fp32"},
+                   "schedule": ("q, k, v (one shared input) concurrently on 3 streams (a third of the SMs each); "
+                                "out, fc1, fc2 in order" if concurrent else "all six layers in order on all SMs"),
+                   "arith": "; ".join(arith)},
+        "step_ms_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
         "us_per_layer": per_layer,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # our kernels per step: per layer the x-digit pass + the fused GEMV (+ 1 fp32->fp16 convert
-        # per column-split, all-reduced layer under TP; row-split layers keep sharded outputs)
-        "gpu_launches": K * (2 * len(layers) + (sum(1 for L in layers if L.get("mode", 0) == 1) if world > 1 else 0)),
+        "gpu_launches": K * sum(launches_per_call(L, world) for L in layers),
         "clocks": clk.summary(),
+        "secondary_configs": secondary,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -564,6 +753,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="q, k, v one after another on all SMs")
+    ap.add_argument("--layout", default="auto", choices=["auto", "tc", "cc"],
+                    help="device layout of the headline layers (auto = choose_layout)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the BASELINE config 2/3/4 per-layer lines")
+    ap.add_argument("--secondary-seconds", type=float, default=60.0)
+    ap.add_argument("--no-quantizer-time", dest="quantizer_time", action="store_false",
+                    help="skip timing the oracle quantizer at config 1 (768x768, k = 8) for cpu_baseline")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -27,7 +27,7 @@ __all__ = [
     "owq_tp_gemv", "OwqLinear", "OWQ_TP_ROWS", "OWQ_TP_COLS", "OWQ_PACK_STRICT",
     "OWQ_PACK_U8_CODES", "OWQ_PACK_LAYOUT_CC", "OWQ_LAYOUT_TC", "OWQ_LAYOUT_CC",
     "owq_packed_bytes_layout", "owq_workspace_bytes_grid", "owq_packed_bytes_colmap", "owq_pack_host_colmap",
-    "owq_pack_colmap", "owq_blob_colmap_host", "EXPORTED_SYMBOLS",
+    "owq_pack_colmap", "owq_blob_colmap_host", "choose_layout", "EXPORTED_SYMBOLS",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -486,19 +486,33 @@ def owq_tp_gemv(tp, mode, full, shard, d_packed, x, y, y_f32=False, ws=None, str
     return y
 
 
+def choose_layout(shape, max_batch: int = 1) -> int:
+    """Device layout to pack a layer for, from the measured crossover on B200
+    (profiles/r2_layout_table.txt): the CUDA-core kernel
+    (layout 4) for batch-1 decode of grouped-scale layers and of layers up to
+    ~48 M weights (lower fixed cost per call); the tcgen05 kernel (layout 3)
+    for larger per-row layers and for batches > 1 (tensor cores)."""
+    s = _shape(shape)
+    if max_batch > 1:
+        return OWQ_LAYOUT_TC
+    if s.group_size > 0 or s.c_out * s.c_in <= 48 * 1024 * 1024:
+        return OWQ_LAYOUT_CC
+    return OWQ_LAYOUT_TC
+
+
 class OwqLinear:
     """A packed OWQ layer resident in HBM: ``y = layer(x)`` (x fp16 [B][c_in])."""
 
     def __init__(self, rep: dict, device=None, max_batch: int = 16, flags: int = 0, layout: int = None):
         """layout: OWQ_LAYOUT_TC (tcgen05 kernel) or OWQ_LAYOUT_CC (CUDA-core kernel);
-        None = OWQ_LAYOUT_CC when max_batch <= 4 (decode), else OWQ_LAYOUT_TC."""
+        None = choose_layout(shape, max_batch)."""
         import torch
         self.shape = _shape((rep["M"], rep["K"], rep["bits"], rep["group"], len(rep["weak_idx"])))
         self.device = torch.device(device or "cuda")
         if self.device.index is None:
             self.device = torch.device("cuda", torch.cuda.current_device())
         if layout is None:
-            layout = OWQ_LAYOUT_CC if max_batch <= 4 else OWQ_LAYOUT_TC
+            layout = choose_layout(self.shape, max_batch)
         if layout == OWQ_LAYOUT_CC:
             flags |= OWQ_PACK_LAYOUT_CC
         self.layout = layout
