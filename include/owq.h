@@ -276,6 +276,39 @@ owq_status owq_tp_gemv(owq_tp *tp, int mode, const owq_shape *full, const owq_sh
 owq_status owq_tp_bounds(const owq_shape *full, int mode, int world, int rank,
                          int32_t *begin, int32_t *end);
 
+/* ---- OWQ quantization on the GPU (off the hot path) ----
+ * The paper's algorithm (DESIGN.md §3 readings s1-s12) in fp64:
+ * H = 2 X X^T (Eq. 3); dead columns H_jj := 1, W[:, j] := 0 and
+ * H += percdamp * mean(diag H) * I; Eq. 5 sensitivity lambda_j ||dW_:,j||^2
+ * with lambda_j the undamped H_jj and dW the min-max RTN error;
+ * the n_weak most sensitive columns (ties -> smaller index) are kept in
+ * fp16 and go last in the OPTQ order; OPTQ (Eq. 1) quantizes the
+ * rest with a truncation-searched grid per row / original group fitted on
+ * the group's current values; weak codes are zero-filled.
+ * Output = the paper representation on the device: codes one per byte
+ * [c_out][c_in] (pack with owq_pack + OWQ_PACK_U8_CODES after a copy),
+ * fp16 scale / zero [c_out][G], u16 weak_idx [n_weak] ascending, fp16
+ * weak_val [c_out][n_weak].  Synchronises the stream once (group runs) and at
+ * the end (status).  UNSUPPORTED: bits outside [2, 8], group_size > 128,
+ * n_weak >= c_in.  INVALID_ARG: NULL buffers, percdamp <= 0, or H not positive
+ * definite after dampening. */
+typedef struct {
+  int32_t bits;         /* b */
+  int32_t group_size;   /* g: 0 = per row, else <= 128 columns (original index groups) */
+  int32_t n_weak;       /* k */
+  int32_t clip;         /* 1 = truncation search over p = 1 - i/100, i < 80; 0 = min-max */
+  double percdamp;      /* 0.01 (reading s2) */
+} owq_quant_params;
+
+size_t owq_quantize_workspace_bytes(int32_t c_out, int32_t c_in, int32_t n_samples,
+                                    const owq_quant_params *params);
+/* d_W: fp64 [c_out][c_in]; d_X: fp64 calibration features [c_in][n_samples]. */
+owq_status owq_quantize_gpu(int32_t c_out, int32_t c_in, int32_t n_samples,
+                            const double *d_W, const double *d_X, const owq_quant_params *params,
+                            uint8_t *d_codes, uint16_t *d_scale, uint16_t *d_zero,
+                            uint16_t *d_weak_idx, uint16_t *d_weak_val,
+                            void *d_workspace, size_t ws_bytes, void *stream);
+
 const char *owq_status_string(owq_status s);
 
 #ifdef __cplusplus

@@ -27,7 +27,8 @@ __all__ = [
     "owq_tp_gemv", "OwqLinear", "OWQ_TP_ROWS", "OWQ_TP_COLS", "OWQ_PACK_STRICT",
     "OWQ_PACK_U8_CODES", "OWQ_PACK_LAYOUT_CC", "OWQ_LAYOUT_TC", "OWQ_LAYOUT_CC",
     "owq_packed_bytes_layout", "owq_workspace_bytes_grid", "owq_packed_bytes_colmap", "owq_pack_host_colmap",
-    "owq_pack_colmap", "owq_blob_colmap_host", "choose_layout", "EXPORTED_SYMBOLS",
+    "owq_pack_colmap", "owq_blob_colmap_host", "choose_layout", "owq_quantize_gpu",
+    "owq_quantize_workspace_bytes", "EXPORTED_SYMBOLS",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -45,6 +46,7 @@ EXPORTED_SYMBOLS = [
     "owq_tp_shard_shape", "owq_tp_shard_host", "owq_tp_shard", "owq_tp_workspace_bytes",
     "owq_tp_gemv", "owq_tp_bounds", "owq_status_string", "owq_packed_bytes_colmap",
     "owq_pack_host_colmap", "owq_pack_colmap", "owq_blob_colmap_host",
+    "owq_quantize_workspace_bytes", "owq_quantize_gpu",
 ]
 
 
@@ -62,6 +64,11 @@ class Shape(ctypes.Structure):
 
     def tup(self):
         return (self.c_out, self.c_in, self.bits, self.group_size, self.n_weak)
+
+
+class _QuantParams(ctypes.Structure):
+    _fields_ = [("bits", ctypes.c_int32), ("group_size", ctypes.c_int32), ("n_weak", ctypes.c_int32),
+                ("clip", ctypes.c_int32), ("percdamp", ctypes.c_double)]
 
 
 class _ColMap(ctypes.Structure):
@@ -121,6 +128,10 @@ def lib():
         "owq_pack_host_colmap": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.POINTER(_ColMap), ctypes.c_int, _P, sz]),
         "owq_pack_colmap": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.POINTER(_ColMap), ctypes.c_int, _P, sz, _P]),
         "owq_blob_colmap_host": (st, [_P, sz, ctypes.POINTER(ctypes.c_int32), _P]),
+        "owq_quantize_workspace_bytes": (sz, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.POINTER(_QuantParams)]),
+        "owq_quantize_gpu": (st, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P,
+                                  ctypes.POINTER(_QuantParams), _P, _P, _P, _P, _P, _P, sz, _P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -484,6 +495,49 @@ def owq_tp_gemv(tp, mode, full, shard, d_packed, x, y, y_f32=False, ws=None, str
                              x.data_ptr(), B, y.data_ptr(), int(bool(y_f32)), ws.data_ptr(),
                              ws.numel(), _stream(stream)))
     return y
+
+
+def owq_quantize_workspace_bytes(c_out: int, c_in: int, n_samples: int, bits: int, n_weak: int,
+                                 group: int = 0, clip: bool = True, percdamp: float = 0.01) -> int:
+    prm = _QuantParams(bits, group, n_weak, int(bool(clip)), percdamp)
+    return int(lib().owq_quantize_workspace_bytes(c_out, c_in, n_samples, ctypes.byref(prm)))
+
+
+def owq_quantize_gpu(W, X, bits: int, n_weak: int, group: int = 0, clip: bool = True, percdamp: float = 0.01,
+                     stream=None) -> dict:
+    """OWQ quantization on the GPU (NEXT-1, owq.h owq_quantize_gpu): W fp64 [c_out][c_in],
+    calibration X fp64 [c_in][n_samples], both contiguous CUDA tensors.  Returns the
+    paper representation as CUDA tensors: codes u8 [M][K], scale_f16 / zero_f16 u16
+    bit patterns [M][G], weak_idx u16 [k], weak_val_f16 u16 [M][k]."""
+    import torch
+    if W.dtype != torch.float64 or X.dtype != torch.float64 or not W.is_cuda or W.device != X.device:
+        raise OwqError("W and X must be float64 CUDA tensors on one device")
+    W, X = W.contiguous(), X.contiguous()
+    M, K = W.shape
+    if X.shape[0] != K:
+        raise OwqError(f"X must be [{K}][n_samples], got {tuple(X.shape)}")
+    N = X.shape[1]
+    G = 1 if group == 0 else -(-K // group)
+    dev = W.device
+    out = {"codes": torch.empty((M, K), dtype=torch.uint8, device=dev),
+           "scale_f16": torch.empty((M, G), dtype=torch.int16, device=dev),
+           "zero_f16": torch.empty((M, G), dtype=torch.int16, device=dev),
+           "weak_idx": torch.empty(max(n_weak, 1), dtype=torch.int16, device=dev),
+           "weak_val_f16": torch.empty((M, max(n_weak, 1)), dtype=torch.int16, device=dev)}
+    prm = _QuantParams(bits, group, n_weak, int(bool(clip)), percdamp)
+    with _on_device(dev):
+        nws = int(lib().owq_quantize_workspace_bytes(M, K, N, ctypes.byref(prm)))
+        if nws == 0:
+            raise OwqError("OWQ_ERR_INVALID_ARG (quantizer shape)")
+        ws = torch.empty(nws, dtype=torch.uint8, device=dev)
+        _check(lib().owq_quantize_gpu(M, K, N, W.data_ptr(), X.data_ptr(), ctypes.byref(prm),
+                                      out["codes"].data_ptr(), out["scale_f16"].data_ptr(),
+                                      out["zero_f16"].data_ptr(), out["weak_idx"].data_ptr(),
+                                      out["weak_val_f16"].data_ptr(), ws.data_ptr(), nws, _stream(stream)))
+    out["weak_idx"] = out["weak_idx"][:n_weak]
+    out["weak_val_f16"] = out["weak_val_f16"][:, :n_weak]
+    out.update(M=M, K=K, bits=bits, group=group)
+    return out
 
 
 def choose_layout(shape, max_batch: int = 1) -> int:

@@ -17,7 +17,7 @@ BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU = ["owq_gemv.cu", "owq_gemv_cc.cu", "owq_tp.cu"]
+CU = ["owq_gemv.cu", "owq_gemv_cc.cu", "owq_tp.cu", "owq_quant.cu"]
 CPP = ["owq_pack.cpp"]
 HDRS = ["owq_layout.h", "owq_layout_cc.h"]
 
