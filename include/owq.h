@@ -218,6 +218,18 @@ owq_status owq_gemm_small_batch(const owq_shape *shape, const void *d_packed,
                                 int y_f32, void *d_workspace, size_t ws_bytes,
                                 void *stream);
 
+/* Prefill: Y = W_hat X for any number of tokens (P:58 X in
+ * R^{C_in x N}), d_x fp16 [n_tokens][c_in] (16-byte aligned, c_in % 8 == 0),
+ * d_y [n_tokens][c_out] (fp32 if y_f32).  Tensor cores: A = the exact integer
+ * (q - z) as fp16 decoded into shared memory, B = x, fp32 accumulation in TMEM
+ * (tcgen05.mma kind::f16, 128 rows x 256 tokens per CTA); s applied per row after
+ * the sum; fp16 weak columns folded in by the epilogue.  Layout 3 blobs with
+ * per-row scales only: UNSUPPORTED for layout 4, group_size > 0 or c_in % 8 != 0.
+ * No workspace. */
+owq_status owq_gemm_prefill(const owq_shape *shape, const void *d_packed,
+                            const uint16_t *d_x, int32_t n_tokens, void *d_y,
+                            int y_f32, void *stream);
+
 /* Test/tuning hook: same as owq_gemm_small_batch with an explicit grid size
  * (number of CTAs; 0 = one per SM; capped at one CTA per item; > 512 after the
  * cap -> UNSUPPORTED).  Small grids exercise the stream-K partial-sum path with

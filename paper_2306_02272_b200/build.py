@@ -17,9 +17,9 @@ BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU = ["owq_gemv.cu", "owq_gemv_cc.cu", "owq_tp.cu", "owq_quant.cu"]
+CU = ["owq_gemv.cu", "owq_gemv_cc.cu", "owq_tp.cu", "owq_quant.cu", "owq_prefill.cu"]
 CPP = ["owq_pack.cpp"]
-HDRS = ["owq_layout.h", "owq_layout_cc.h"]
+HDRS = ["owq_layout.h", "owq_layout_cc.h", "owq_ptx.cuh"]
 
 
 def nccl_dirs():

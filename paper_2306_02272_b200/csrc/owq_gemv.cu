@@ -54,6 +54,9 @@ owq_status unpack(const Geo& g, const void* blob, uint8_t* codes, cudaStream_t s
 int grid_for(const Geo& g, int grid_req);
 size_t workspace_bytes(int grid, int nb);
 }  // namespace cc
+namespace pf {   // owq_prefill.cu
+owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, cudaStream_t stream);
+}  // namespace pf
 }  // namespace owq
 
 namespace owq {
@@ -1751,6 +1754,19 @@ owq_status owq_gemv(const owq_shape* s, const void* d_packed, const uint16_t* d_
 owq_status owq_gemm_small_batch(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int batch, void* d_y,
                                 int y_f32, void* d_ws, size_t ws_bytes, void* stream) {
   return gemm_impl(s, d_packed, d_x, batch, d_y, y_f32, d_ws, ws_bytes, 0, stream);
+}
+
+owq_status owq_gemm_prefill(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int32_t n_tokens, void* d_y,
+                            int y_f32, void* stream) {
+  if (!d_x || !d_y) return OWQ_ERR_INVALID_ARG;
+  if (n_tokens < 1) return OWQ_ERR_INVALID_ARG;
+  int layout = 0, Ks = -1;
+  owq_status st = blob_layout(s, d_packed, (cudaStream_t)stream, layout, Ks);
+  if (st != OWQ_OK) return st;
+  if (layout != OWQ_LAYOUT_VERSION || s->group_size != 0 || (s->c_in & 7)) return OWQ_ERR_UNSUPPORTED;
+  if (reinterpret_cast<uintptr_t>(d_x) & 15) return OWQ_ERR_INVALID_ARG;
+  return pf::launch(make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak), d_packed, d_x, n_tokens, d_y, y_f32,
+                    (cudaStream_t)stream);
 }
 
 owq_status owq_gemm_small_batch_grid(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int batch,

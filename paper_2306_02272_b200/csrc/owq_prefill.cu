@@ -1,0 +1,331 @@
+// owq_prefill.cu -- the mixed OWQ matmul for many tokens (SURVEY §8(f) NEXT-2,
+// "prefill"): Y = W_hat X with X = B tokens x C_in (X in R^{C_in x N};
+// the same representation as the GEMV), B = 17 .. any, per-row scales,
+// blob layout 3 (the tensor-core layout of the GEMV).
+//
+// At 64-2048 tokens the product is a dense contraction (2 B flops per code
+// byte x 8/3), so it runs on the 5th-generation tensor cores:
+//   A (weights)  = the EXACT integer (q - z) as fp16 (|q - z| <= 15), decoded
+//                  from the packed codes by 4 warps (thread = row): the layout-3
+//                  LOP3 decode to code bytes, one PRMT per 2 codes that places
+//                  them under the 1024 fp16 exponent (1024 + q), one HSUB2 of
+//                  1024 + z -- written to shared memory in the UMMA K-major
+//                  core-matrix layout;
+//   B (tokens)   = x fp16 as given, cp.async'ed into the same layout;
+//   D            = fp32 in TMEM (128 rows x 256 tokens), tcgen05.mma.kind::f16,
+//                  4 MMAs (K = 16) per 64-column super-step, one issuing thread.
+// fp16 x fp16 products are exact in the fp32 accumulator; the scale s is
+// applied once per row after the sum (reading s19: never an fp16-rounded
+// s (q - z), SURVEY §8(c) scheme D).  The fp16 weak columns are folded in by
+// the epilogue (fp16 x fp16 in fp32).
+//
+// Tile: one CTA = two 128-row blocks (sharing one x tile; two D accumulators
+// fill the 512 TMEM columns) x 256 tokens; grid = (token tiles, row-block
+// pairs), token tile fastest so the CTAs sharing weights run together and read
+// the codes from L2.  3-stage ring: codes (TMA bulk), A tiles (8 decode warps,
+// which are also the epilogue), B tile (4 loader warps, cp.async groups with
+// one stage of lookahead); the MMA warp commits each stage's MMAs to the
+// stage's `empty` barrier.  Measured 385-425 dense-equivalent TFLOP/s at 1-2k
+// tokens (profiles/r2_prefill_time.txt): bound by moving the x tile through
+// L2 with cp.async, not by the tensor cores.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "owq.h"
+#include "owq_layout.h"
+#include "owq_ptx.cuh"
+
+namespace owq {
+namespace pf {
+
+using namespace owq::ptx;
+
+constexpr int NT = 256;                  // tokens per CTA (MMA N)
+constexpr int RB = 2;                    // 128-row blocks per CTA (share the x tile)
+constexpr int NST = 3;                   // pipeline stages
+constexpr uint32_t A_BYTES = 128 * 64 * 2;       // 16 KB per row-block: [8 K-chunks][16 row groups][8 rows][16 B]
+constexpr uint32_t B_BYTES = NT * 64 * 2;        // 32 KB: [8 K-chunks][NT/8 groups][8 rows][16 B]
+constexpr uint32_t C_MAX = 128 * 8 * 4;          // codes of one row-block super-step (4-bit: 8 words per row)
+constexpr uint32_t STAGE = RB * A_BYTES + B_BYTES + RB * C_MAX;
+constexpr int kDecW = 4 * RB;            // decode (then epilogue) warps: thread = row
+constexpr int kLoadW = 4;                // x loader warps
+constexpr int kProdW = kDecW + kLoadW, kMmaW = kProdW + 1;
+constexpr int kThreads = (kMmaW + 1) * 32;
+constexpr uint32_t kSmem = NST * STAGE + 1024 + 256;
+
+struct Params {
+  const uint8_t* blob;
+  const __half* x;     // [B][K]
+  void* y;             // [B][M]
+  Geo g;
+  int32_t B, y_f32;
+};
+
+// one row's 64 codes of a super-step -> 16 words of 4 code bytes (layout 3)
+template <int BITS>
+__device__ __forceinline__ void decode_row(const uint32_t* w, uint32_t* o) {
+  if (BITS == 4) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      o[i] = w[i] & 0x0F0F0F0Fu;
+      o[8 + i] = (w[i] >> 4) & 0x0F0F0F0Fu;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      o[i] = w[i] & 0x07070707u;
+      o[6 + i] = (w[i] >> 3) & 0x07070707u;
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      o[12 + r] = ((w[r] >> 6) & 0x03030303u) | ((w[4 + (r >> 1)] >> ((r & 1) ? 5 : 4)) & 0x04040404u);
+  }
+}
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+template <int BITS>
+__global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const Geo& g = p.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x, rb0 = blockIdx.y * RB;
+  const int nss = g.nss;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + NST * STAGE);
+  uint64_t* full = bars;               // codes landed (TMA tx)
+  uint64_t* afull = full + NST;        // A tiles written (RB x 128 threads)
+  uint64_t* bfull = afull + NST;       // B tile written (loader lanes)
+  uint64_t* empty = bfull + NST;       // the stage's MMAs completed (tcgen05.commit)
+  uint64_t* dfull = empty + NST;       // all MMAs completed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + 1);
+  auto A = [&](int s, int h) { return base + (size_t)s * STAGE + (size_t)h * A_BYTES; };
+  auto Bt = [&](int s) { return base + (size_t)s * STAGE + RB * A_BYTES; };
+  auto Cd = [&](int s, int h) { return base + (size_t)s * STAGE + RB * A_BYTES + B_BYTES + (size_t)h * C_MAX; };
+  const int nrb_here = min(RB, g.nrb - rb0);   // row-blocks of this CTA (the last CTA may have one)
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&afull[s], RB * 128);
+      mbar_init(&bfull[s], kLoadW * 32);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(dfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProdW) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t ssb = (uint32_t)g.ss_bytes;
+
+  if (warp == kProdW) {
+    // ------------------------------------------------ producer: codes of each super-step (TMA bulk)
+    if (lane == 0) {
+      pdl_launch_dependents();
+      for (int ss = 0; ss < nss; ++ss) {
+        const int s = ss % NST;
+        if (ss >= NST) mbar_wait(&empty[s], (uint32_t)((ss / NST) - 1) & 1u);
+        mbar_expect_tx(&full[s], ssb * nrb_here);
+        for (int h = 0; h < nrb_here; ++h)
+          bulk_g2s(Cd(s, h), p.blob + g.units_off + item_offset(g, rb0 + h, ss), ssb, &full[s]);
+      }
+    }
+  } else if (warp == kMmaW) {
+    // ------------------------------------------------ MMA issue (one thread): per row-block h,
+    // D_h (TMEM columns 256 h ..) += A_h x B
+    constexpr uint32_t idesc = idesc_f16(128, NT);
+    for (int ss = 0; ss < nss; ++ss) {
+      const int s = ss % NST;
+      const uint32_t ph = (uint32_t)(ss / NST) & 1u;
+      mbar_wait(&afull[s], ph);
+      mbar_wait(&bfull[s], ph);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t b0 = smem_u32(Bt(s));
+        for (int h = 0; h < nrb_here; ++h) {
+          const uint32_t a0 = smem_u32(A(s, h));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)   // K = 16 per MMA = two 8-element core-matrix columns
+            tc_mma_f16_ss(tmem + (uint32_t)(h * NT), umma_desc(a0 + kk * 2 * 2048, 2048, 128),
+                          umma_desc(b0 + kk * 2 * (NT * 16), NT * 16, 128), idesc, (ss | kk) != 0 ? 1u : 0u);
+        }
+        tc_commit(&empty[s]);
+        if (ss == nss - 1) tc_commit(dfull);
+      }
+      __syncwarp();
+    }
+  } else if (warp < kDecW) {
+    // ------------------------------------------------ decode: thread = weight row of row-block h
+    const int h = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const int rb = rb0 + h;
+    const bool live = h < nrb_here;
+    const uint32_t szw = live ? __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off + (int64_t)rb * kSZBlockBytes) + r) : 0u;
+    const float z = __high2float(*reinterpret_cast<const __half2*>(&szw));
+    const __half2 zz = __float2half2_rn(1024.f + z);   // exact: z <= 15
+    const uint32_t zzw = *reinterpret_cast<const uint32_t*>(&zz);
+    constexpr int WPR = BITS == 3 ? 6 : 8;
+    for (int ss = 0; ss < nss; ++ss) {
+      const int s = ss % NST;
+      mbar_wait(&full[s], (uint32_t)(ss / NST) & 1u);
+      if (!live) {          // the CTA's second row-block does not exist: nothing to decode
+        mbar_arrive(&afull[s]);
+        continue;
+      }
+      const uint8_t* rec = Cd(s, h);
+      uint32_t w[8], o[16];
+#pragma unroll
+      for (int i = 0; i < WPR; ++i) w[i] = *reinterpret_cast<const uint32_t*>(rec + row_word_byte(BITS, r, i));
+      decode_row<BITS>(w, o);
+      const uint32_t arow = smem_u32(A(s, h)) + (uint32_t)(r >> 3) * 128u + (uint32_t)(r & 7) * 16u;
+#pragma unroll
+      for (int kc = 0; kc < 8; ++kc) {   // columns 8kc .. 8kc+7 = code words 2kc, 2kc+1
+        const uint32_t w0 = o[2 * kc], w1 = o[2 * kc + 1];
+        const uint32_t h0 = hsub2(prmt(w0, 0x64646464u, 0x4140u), zzw);   // (q - z) of columns 8kc, 8kc+1
+        const uint32_t h1 = hsub2(prmt(w0, 0x64646464u, 0x4342u), zzw);
+        const uint32_t h2 = hsub2(prmt(w1, 0x64646464u, 0x4140u), zzw);
+        const uint32_t h3 = hsub2(prmt(w1, 0x64646464u, 0x4342u), zzw);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(arow + kc * 2048u), "r"(h0), "r"(h1), "r"(h2),
+                     "r"(h3)
+                     : "memory");
+      }
+      fence_proxy_async();
+      mbar_arrive(&afull[s]);
+    }
+    // ---- epilogue (the decode warps): thread = row, TMEM lane quarter = warp % 4, D_h
+    if (!live) goto done;
+    {
+    const int q = warp & 3;
+    const int64_t tok0 = (int64_t)tile * NT;
+    const int64_t grow = (int64_t)rb * kRowBlock + r;
+    const uint32_t szw = __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off + (int64_t)rb * kSZBlockBytes) + r);
+    const float sc = __low2float(*reinterpret_cast<const __half2*>(&szw));
+    pdl_wait();   // y (and x) belong to earlier kernels until they complete
+    mbar_wait(dfull, 0);
+    tc_fence_after();
+    const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
+    const uint8_t* wrec = p.blob + g.units_off + (int64_t)rb * g.rb_bytes + (int64_t)g.nss * g.ss_bytes;
+    for (int c16 = 0; c16 < NT / 16; ++c16) {
+      uint32_t d[16];
+      tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16), d);
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = sc * __uint_as_float(d[j]);
+      // fp16 weak columns x the tokens' fp16 activations at their indices
+      for (int tt = 0; tt < g.k; ++tt) {
+        const int ch = tt / kWeakChunk, c = tt % kWeakChunk;
+        const __half wv = ch < g.nfull
+                              ? *reinterpret_cast<const __half*>(wrec + (int64_t)ch * kWeakChunkBytes + (r * kWeakChunk + c) * 2)
+                              : *reinterpret_cast<const __half*>(wrec + (int64_t)g.nfull * kWeakChunkBytes + (r * g.ktail + c) * 2);
+        const float wf = __half2float(wv);
+        const int j = __ldg(widx + tt);
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int64_t n = tok0 + c16 * 16 + jj;
+          if (n < p.B) v[jj] = fmaf(wf, __half2float(p.x[n * g.K + j]), v[jj]);
+        }
+      }
+      if (grow < g.M)
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const int64_t n = tok0 + c16 * 16 + jj;
+          if (n < p.B) {
+            if (p.y_f32) reinterpret_cast<float*>(p.y)[n * g.M + grow] = v[jj];
+            else reinterpret_cast<__half*>(p.y)[n * g.M + grow] = __float2half_rn(v[jj]);
+          }
+        }
+    }
+    }
+  } else if (warp < kProdW) {
+    // ------------------------------------------------ x loaders: cp.async, NST - 1 stages in flight
+    const int t = threadIdx.x - kDecW * 32;
+    constexpr int LT = kLoadW * 32;
+    const int64_t tok0 = (int64_t)tile * NT;
+    pdl_wait();   // x belongs to earlier kernels until they complete
+    for (int ss = 0; ss < nss; ++ss) {
+      const int s = ss % NST;
+      if (ss >= NST) mbar_wait(&empty[s], (uint32_t)((ss / NST) - 1) & 1u);
+      const uint32_t b0 = smem_u32(Bt(s));
+#pragma unroll 4
+      for (int e = t; e < NT * 8; e += LT) {   // 16-byte chunks: token n, K-chunk kc
+        const int n = e >> 3, kc = e & 7;
+        const int64_t col = (int64_t)ss * 64 + kc * 8;
+        const bool ok = tok0 + n < p.B && col < g.K;
+        const __half* src = ok ? p.x + (tok0 + n) * g.K + col : p.x;
+        cp_async16(b0 + (uint32_t)kc * (NT * 16) + (uint32_t)(n >> 3) * 128u + (uint32_t)(n & 7) * 16u, src, ok ? 16u : 0u);
+      }
+      cp_async_commit();
+      if (ss >= NST - 2) {   // the group of stage ss - (NST - 2) has landed: publish it
+        asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory");
+        fence_proxy_async();
+        mbar_arrive(&bfull[(ss - (NST - 2)) % NST]);
+      }
+    }
+    cp_async_wait_all();
+    fence_proxy_async();
+    for (int ss = (nss > NST - 2 ? nss - (NST - 2) : 0); ss < nss; ++ss) mbar_arrive(&bfull[ss % NST]);
+  }
+done:
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kProdW) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, cudaStream_t stream) {
+  Params p{};
+  p.blob = (const uint8_t*)blob;
+  p.x = (const __half*)x;
+  p.y = y;
+  p.g = g;
+  p.B = B;
+  p.y_f32 = y_f32 ? 1 : 0;
+  auto kern = g.bits == 3 ? owq_prefill_kernel<3> : owq_prefill_kernel<4>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool configured[2][16] = {};
+  if (!configured[g.bits == 3][dev & 15]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess)
+      return OWQ_ERR_CUDA;
+    configured[g.bits == 3][dev & 15] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)((B + NT - 1) / NT), (unsigned)((g.nrb + RB - 1) / RB));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "owq: launch of owq_prefill_kernel failed: %s\n", cudaGetErrorString(e));
+    return OWQ_ERR_CUDA;
+  }
+  return OWQ_OK;
+}
+
+}  // namespace pf
+}  // namespace owq

@@ -1,0 +1,78 @@
+"""Prefill GEMM (owq_gemm_prefill: tcgen05 kind::f16 with the exact
+integer (q - z) as the fp16 A operand) against the fp64 oracle: full outputs where
+the oracle finishes in seconds, sampled rows at OPT-175B width; token counts that
+leave ragged tiles (17, 300) and span several tiles (2048)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from owq_testutil import TOL, rel_err, rep_from_synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2306_02272_b200 as owq  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    return torch.device("cuda:0")
+
+
+def run(d, x, dev, y_f32=True):
+    L = owq.OwqLinear(d, device=dev, layout=owq.OWQ_LAYOUT_TC)
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float16)).to(dev)
+    y = owq.owq_gemm_prefill(L.shape, L.packed, xt, y_f32=y_f32)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("M,K,bits,k,B", [
+    (768, 768, 3, 8, 64), (768, 768, 3, 8, 17), (300, 1000, 4, 5, 300), (1000, 2048, 3, 0, 256),
+    (4096, 4096, 3, 5, 512), (130, 640, 3, 9, 2048),
+])
+def test_prefill_full_parity(dev, M, K, bits, k, B):
+    d = synth.representation(M, K, bits, 0, k, seed=M + K + B)
+    x = synth.activations(B, K, seed=B, outliers=d["weak_idx"])
+    y = run(d, x, dev)
+    e, eu = rel_err(y, O.matvec(rep_from_synth(d), x.astype(np.float64)))
+    assert e <= TOL, (e, eu)
+
+
+@pytest.mark.parametrize("M,K,k", [(12288, 12288, 15), (49152, 12288, 3)])
+def test_prefill_opt175b_sampled(dev, M, K, k):
+    d = synth.representation(M, K, 3, 0, k, seed=M)
+    B = 256
+    x = synth.activations(B, K, seed=3, outliers=d["weak_idx"][:8])
+    y = run(d, x, dev)
+    r = np.random.default_rng(1)
+    rows = sorted(set([0, 127, 128, M - 1] + list(r.choice(M, 60, replace=False))))
+    ref = O.matvec_rows(rep_from_synth(d), x.astype(np.float64), rows)
+    e, eu = rel_err(y[:, rows], ref)
+    assert e <= TOL, (e, eu)
+
+
+def test_prefill_fp16_out_and_probes(dev):
+    # x = e_j probes: non-weak j -> s (q - z) exactly; weak j -> v exactly (fp32 out)
+    M, K, k = 256, 512, 4
+    d = synth.representation(M, K, 3, 0, k, seed=7)
+    js = list(d["weak_idx"]) + [0, 1, 63, 64, 255, 511]
+    X = np.zeros((len(js), K), np.float16)
+    for n, j in enumerate(js):
+        X[n, j] = 1.0
+    y = run(d, X, dev)
+    assert np.array_equal(y, O.matvec(rep_from_synth(d), X.astype(np.float64)))
+    x = synth.activations(33, K, seed=2, outliers=d["weak_idx"])
+    y16 = run(d, x, dev, y_f32=False)
+    assert rel_err(y16, O.matvec(rep_from_synth(d), x.astype(np.float64)))[0] <= TOL
+
+
+def test_prefill_unsupported(dev):
+    d = synth.representation(128, 256, 4, 128, 2, seed=1)
+    L = owq.OwqLinear(d, device=dev, layout=owq.OWQ_LAYOUT_TC)
+    x = torch.zeros((32, 256), dtype=torch.float16, device=dev)
+    with pytest.raises(owq.OwqError, match="UNSUPPORTED"):
+        owq.owq_gemm_prefill(L.shape, L.packed, x)
