@@ -218,6 +218,17 @@ owq_status owq_gemm_small_batch(const owq_shape *shape, const void *d_packed,
                                 int y_f32, void *d_workspace, size_t ws_bytes,
                                 void *stream);
 
+/* Batched GEMV on tensor cores with an exact fp16 A operand:
+ * Y = W_hat X for batch in [1, 32], layout-3 blobs, per-row or grouped scales
+ * (group_size a multiple of 64), c_in % 8 == 0, d_x 16-byte aligned.  A = the
+ * exact integer (q - z) as fp16 in shared memory, B = x (N = batch padded to
+ * 16 / 32), fp32 D in TMEM, one D per scale group drained by s_g; K split over
+ * the grid with a deterministic last-arriver sum.  Workspace: the GEMV
+ * workspace (owq_workspace_bytes with batch >= 2). */
+owq_status owq_gemm_batch_f16(const owq_shape *shape, const void *d_packed,
+                              const uint16_t *d_x, int batch, void *d_y, int y_f32,
+                              void *d_workspace, size_t ws_bytes, void *stream);
+
 /* Prefill: Y = W_hat X for any number of tokens (P:58 X in
  * R^{C_in x N}), d_x fp16 [n_tokens][c_in] (16-byte aligned, c_in % 8 == 0),
  * d_y [n_tokens][c_out] (fp32 if y_f32).  Tensor cores: A = the exact integer

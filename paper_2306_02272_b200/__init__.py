@@ -28,7 +28,7 @@ __all__ = [
     "OWQ_PACK_U8_CODES", "OWQ_PACK_LAYOUT_CC", "OWQ_LAYOUT_TC", "OWQ_LAYOUT_CC",
     "owq_packed_bytes_layout", "owq_workspace_bytes_grid", "owq_packed_bytes_colmap", "owq_pack_host_colmap",
     "owq_pack_colmap", "owq_blob_colmap_host", "choose_layout", "owq_quantize_gpu",
-    "owq_quantize_workspace_bytes", "owq_gemm_prefill", "EXPORTED_SYMBOLS",
+    "owq_quantize_workspace_bytes", "owq_gemm_prefill", "owq_gemm_batch_f16", "EXPORTED_SYMBOLS",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -46,7 +46,7 @@ EXPORTED_SYMBOLS = [
     "owq_tp_shard_shape", "owq_tp_shard_host", "owq_tp_shard", "owq_tp_workspace_bytes",
     "owq_tp_gemv", "owq_tp_bounds", "owq_status_string", "owq_packed_bytes_colmap",
     "owq_pack_host_colmap", "owq_pack_colmap", "owq_blob_colmap_host",
-    "owq_quantize_workspace_bytes", "owq_quantize_gpu", "owq_gemm_prefill",
+    "owq_quantize_workspace_bytes", "owq_quantize_gpu", "owq_gemm_prefill", "owq_gemm_batch_f16",
 ]
 
 
@@ -129,6 +129,7 @@ def lib():
         "owq_pack_colmap": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.POINTER(_ColMap), ctypes.c_int, _P, sz, _P]),
         "owq_blob_colmap_host": (st, [_P, sz, ctypes.POINTER(ctypes.c_int32), _P]),
         "owq_gemm_prefill": (st, [_S, _P, _P, ctypes.c_int32, _P, ctypes.c_int, _P]),
+        "owq_gemm_batch_f16": (st, [_S, _P, _P, ctypes.c_int, _P, ctypes.c_int, _P, sz, _P]),
         "owq_quantize_workspace_bytes": (sz, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                               ctypes.POINTER(_QuantParams)]),
         "owq_quantize_gpu": (st, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _P, _P,
@@ -411,6 +412,20 @@ def owq_gemm_small_batch(shape, d_packed, x, y=None, y_f32=False, ws=None, strea
         _check(lib().owq_gemm_small_batch(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B,
                                           y.data_ptr(), int(bool(y_f32)), ws.data_ptr(), ws.numel(),
                                           _stream(stream)))
+    return y
+
+
+def owq_gemm_batch_f16(shape, d_packed, x, y=None, y_f32=False, ws=None, stream=None):
+    """Y = W_hat X for fp16 X [B][c_in], B in [1, 32], on tensor cores with the exact
+    (q - z) fp16 A operand (layout-3 blobs)."""
+    s = _shape(shape)
+    B = x.shape[0] if x.dim() == 2 else 1
+    y = _out(s, B, y, y_f32, x.device)
+    _check_io(s, d_packed, x, y, y_f32, B, ws)
+    with _on_device(d_packed.device):
+        ws = ws if ws is not None else workspace(s, min(max(B, 2), 16), x.device)
+        _check(lib().owq_gemm_batch_f16(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B, y.data_ptr(),
+                                        int(bool(y_f32)), ws.data_ptr(), ws.numel(), _stream(stream)))
     return y
 
 

@@ -56,6 +56,11 @@ size_t workspace_bytes(int grid, int nb);
 }  // namespace cc
 namespace pf {   // owq_prefill.cu
 owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, cudaStream_t stream);
+namespace sb {
+owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, void* ws,
+                  size_t ws_bytes, int sms, cudaStream_t stream);
+size_t workspace_bytes(const Geo& g, int B, int sms);
+}  // namespace sb
 }  // namespace pf
 }  // namespace owq
 
@@ -1740,8 +1745,9 @@ size_t owq_workspace_bytes_grid(const owq_shape* s, int batch, int grid) {
   // an upper bound for any n_weak: the requested grid before the per-shape cap
   const int64_t G = grid > 0 ? grid : device_sms();
   if (G > kMaxGrid) return 0;
-  // one workspace serves either layout of the layer
-  return std::max(ws_bytes_for(g, batch, G), cc::workspace_bytes((int)G, std::min(batch, 4)));
+  // one workspace serves either layout of the layer and the small-batch f16 kernel
+  const size_t sbw = ws_sync() + pf::sb::workspace_bytes(g, 32, device_sms());   // any batch <= 32
+  return std::max(std::max(ws_bytes_for(g, batch, G), cc::workspace_bytes((int)G, std::min(batch, 4))), sbw);
 }
 
 size_t owq_workspace_bytes(const owq_shape* s, int batch) { return owq_workspace_bytes_grid(s, batch, 0); }
@@ -1754,6 +1760,20 @@ owq_status owq_gemv(const owq_shape* s, const void* d_packed, const uint16_t* d_
 owq_status owq_gemm_small_batch(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int batch, void* d_y,
                                 int y_f32, void* d_ws, size_t ws_bytes, void* stream) {
   return gemm_impl(s, d_packed, d_x, batch, d_y, y_f32, d_ws, ws_bytes, 0, stream);
+}
+
+owq_status owq_gemm_batch_f16(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int batch, void* d_y,
+                              int y_f32, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_x || !d_y || !d_ws) return OWQ_ERR_INVALID_ARG;
+  if (batch < 1 || batch > 32) return OWQ_ERR_UNSUPPORTED;
+  int layout = 0, Ks = -1;
+  owq_status st = blob_layout(s, d_packed, (cudaStream_t)stream, layout, Ks);
+  if (st != OWQ_OK) return st;
+  if (layout != OWQ_LAYOUT_VERSION || (s->c_in & 7)) return OWQ_ERR_UNSUPPORTED;
+  if (reinterpret_cast<uintptr_t>(d_x) & 15) return OWQ_ERR_INVALID_ARG;
+  if (ws_bytes < ws_sync()) return OWQ_ERR_BUFFER_TOO_SMALL;
+  return pf::sb::launch(make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak), d_packed, d_x, batch, d_y, y_f32,
+                        (uint8_t*)d_ws + ws_sync(), ws_bytes - ws_sync(), device_sms(), (cudaStream_t)stream);
 }
 
 owq_status owq_gemm_prefill(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int32_t n_tokens, void* d_y,

@@ -327,5 +327,353 @@ owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void
   return OWQ_OK;
 }
 
+// ============================================================================
+// Small-batch tensor-core GEMM (B = 2 .. 32): the same A
+// operand as the prefill -- the exact integer (q - z) as fp16 decoded into
+// shared memory -- against x as the fp16 B operand with N = B padded to 16 /
+// 32, so the MMA work per code does not grow with a digit expansion and TMEM
+// holds only the small D accumulators.  Grouped scales: one D buffer per scale
+// group (4 buffers in rotation); the epilogue warps drain a group's D into
+// fp32 registers as tot += s_g D_g while the MMAs run on the next group.  The
+// machine is filled by splitting K over the grid (split boundaries on group
+// boundaries); partial rows go to the workspace and the last-arriving split of
+// a row-block sums them in split order (deterministic), then resets its counter.
+// ============================================================================
+namespace sb {
+
+constexpr int NST = 4;
+#ifndef OWQ_SB_SUB
+#define OWQ_SB_SUB 1
+#endif
+// super-steps per stage: 1 measured faster than 2 (8 decode warps; both are
+// bound by shared-memory traffic: A is written and read as 2 B per code,
+// DESIGN.md §6.5)
+constexpr int SUB = OWQ_SB_SUB;
+constexpr uint32_t A_BYTES = 128 * 64 * 2;
+constexpr uint32_t C_MAX = 128 * 8 * 4;
+constexpr int NDB = 4;                  // D buffers (grouped scales)
+// warps: 0-7 decode (4 per sub-step, thread = row), 8-11 epilogue, 12 x loader, 13 producer, 14 MMA
+constexpr int kDec = 4 * SUB, kEpi0 = kDec, kLoad = kEpi0 + 4, kProd = kLoad + 1, kMma = kProd + 1;
+constexpr int kThreads = (kMma + 1) * 32;
+
+struct Params {
+  const uint8_t* blob;
+  const __half* x;      // [B][K]
+  void* y;              // [B][M]
+  float* part;          // [KS][B][Mp] fp32 partial rows (KS > 1)
+  uint32_t* counters;   // [nrb], zero between calls
+  Geo g;
+  int32_t B, y_f32, KS, sps;   // splits, super-steps per split (a multiple of SUB)
+  int32_t gss;          // super-steps per scale group (0 = per-row scales; else a multiple of SUB)
+};
+
+template <int NT>
+__host__ __device__ constexpr uint32_t stage_bytes() { return SUB * (A_BYTES + NT * 128 + C_MAX); }
+
+template <int BITS, int NT>
+__global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr uint32_t STG = stage_bytes<NT>();
+  const Geo& g = p.g;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int split = blockIdx.x, rb = blockIdx.y;
+  const int ss0 = split * p.sps, ss1 = min(g.nss, ss0 + p.sps);
+  const int nsteps = ss1 - ss0;                  // super-steps of this split
+  const int n = (nsteps + SUB - 1) / SUB;        // stages
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + NST * STG);
+  uint64_t* afull = full + NST;
+  uint64_t* bfull = afull + NST;
+  uint64_t* empty = bfull + NST;
+  uint64_t* dfull = empty + NST;      // [NDB]
+  uint64_t* dempty = dfull + NDB;     // [NDB]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + NDB);
+  int* flag = reinterpret_cast<int*>(tslot + 1);
+  auto A = [&](int s, int u) { return base + (size_t)s * STG + (size_t)u * A_BYTES; };
+  auto Bt = [&](int s, int u) { return base + (size_t)s * STG + SUB * A_BYTES + (size_t)u * (NT * 128); };
+  auto Cd = [&](int s) { return base + (size_t)s * STG + SUB * (A_BYTES + NT * 128); };
+  const bool grouped = p.gss > 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&afull[s], kDec * 32);
+      mbar_init(&bfull[s], 32);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < NDB; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProd) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t ssb = (uint32_t)g.ss_bytes;
+  // scale group of stage l (stages never straddle a group: gss is a multiple of SUB)
+  auto grp = [&](int l) { return grouped ? (ss0 + SUB * l) / p.gss : 0; };
+  auto nsub = [&](int l) { return min(SUB, nsteps - SUB * l); };
+
+  if (warp == kProd) {
+    if (lane == 0) {
+      pdl_launch_dependents();
+      for (int l = 0; l < n; ++l) {
+        const int s = l % NST;
+        if (l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
+        const uint32_t bytes = ssb * (uint32_t)nsub(l);   // consecutive super-steps are contiguous in the blob
+        mbar_expect_tx(&full[s], bytes);
+        bulk_g2s(Cd(s), p.blob + g.units_off + item_offset(g, rb, ss0 + SUB * l), bytes, &full[s]);
+      }
+    }
+  } else if (warp == kMma) {
+    constexpr uint32_t idesc = idesc_f16(128, NT);
+    int gcount = 0;
+    for (int l = 0; l < n; ++l) {
+      const int s = l % NST;
+      const uint32_t ph = (uint32_t)(l / NST) & 1u;
+      const bool first = l == 0 || grp(l) != grp(l - 1);
+      const bool last = l == n - 1 || grp(l) != grp(l + 1);
+      const int buf = grouped ? gcount % NDB : 0;
+      if (first && grouped && gcount >= NDB) mbar_wait(&dempty[buf], (uint32_t)((gcount / NDB) - 1) & 1u);
+      mbar_wait(&afull[s], ph);
+      mbar_wait(&bfull[s], ph);
+      tc_fence_after();
+      if (lane == 0) {
+        const int nu = nsub(l);
+        for (int u = 0; u < nu; ++u) {
+          const uint32_t a0 = smem_u32(A(s, u)), b0 = smem_u32(Bt(s, u));
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_f16_ss(tmem + (uint32_t)(buf * NT), umma_desc(a0 + kk * 2 * 2048, 2048, 128),
+                          umma_desc(b0 + kk * 2 * (NT * 16), NT * 16, 128), idesc, (first && u == 0 && kk == 0) ? 0u : 1u);
+        }
+        tc_commit(&empty[s]);
+        if (last) tc_commit(&dfull[buf]);
+      }
+      __syncwarp();
+      if (last) ++gcount;
+    }
+  } else if (warp < kDec) {
+    // decode: warps 4u .. 4u+3 decode sub-step u of each stage, thread = row; A = (q - z_group) fp16
+    const int u = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    constexpr int WPR = BITS == 3 ? 6 : 8;
+    uint32_t zzw = 0;
+    int zg = -1;
+    for (int l = 0; l < n; ++l) {
+      const int s = l % NST;
+      const int gi = grp(l);
+      if (gi != zg) {
+        const uint32_t szw = __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off +
+                                                                      ((int64_t)rb * g.G + gi) * kSZBlockBytes) + r);
+        const __half2 zz = __float2half2_rn(1024.f + __high2float(*reinterpret_cast<const __half2*>(&szw)));
+        zzw = *reinterpret_cast<const uint32_t*>(&zz);
+        zg = gi;
+      }
+      mbar_wait(&full[s], (uint32_t)(l / NST) & 1u);
+      if (u < nsub(l)) {
+        const uint8_t* rec = Cd(s) + (size_t)u * ssb;
+        uint32_t w[8], o[16];
+#pragma unroll
+        for (int i = 0; i < WPR; ++i) w[i] = *reinterpret_cast<const uint32_t*>(rec + row_word_byte(BITS, r, i));
+        pf::decode_row<BITS>(w, o);
+        const uint32_t arow = smem_u32(A(s, u)) + (uint32_t)(r >> 3) * 128u + (uint32_t)(r & 7) * 16u;
+#pragma unroll
+        for (int kc = 0; kc < 8; ++kc) {
+          const uint32_t w0 = o[2 * kc], w1 = o[2 * kc + 1];
+          const uint32_t h0 = pf::hsub2(pf::prmt(w0, 0x64646464u, 0x4140u), zzw);
+          const uint32_t h1 = pf::hsub2(pf::prmt(w0, 0x64646464u, 0x4342u), zzw);
+          const uint32_t h2 = pf::hsub2(pf::prmt(w1, 0x64646464u, 0x4140u), zzw);
+          const uint32_t h3 = pf::hsub2(pf::prmt(w1, 0x64646464u, 0x4342u), zzw);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(arow + kc * 2048u), "r"(h0), "r"(h1), "r"(h2),
+                       "r"(h3)
+                       : "memory");
+        }
+        fence_proxy_async();
+      }
+      mbar_arrive(&afull[s]);
+    }
+  } else if (warp == kLoad) {
+    // x loader: NT tokens x (SUB x 64) columns per stage (zero rows past B), 2 stages of lookahead
+    pdl_wait();
+    for (int l = 0; l < n; ++l) {
+      const int s = l % NST;
+      if (l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
+#pragma unroll
+      for (int e = lane; e < SUB * NT * 8; e += 32) {
+        const int u = e / (NT * 8), e2 = e % (NT * 8);
+        const int t = e2 >> 3, kc = e2 & 7;
+        const int64_t col = (int64_t)(ss0 + SUB * l + u) * 64 + kc * 8;
+        const bool ok = t < p.B && col < g.K && SUB * l + u < nsteps;
+        cp_async16(smem_u32(Bt(s, u)) + (uint32_t)kc * (NT * 16) + (uint32_t)(t >> 3) * 128u + (uint32_t)(t & 7) * 16u,
+                   ok ? p.x + (int64_t)t * g.K + col : p.x, ok ? 16u : 0u);
+      }
+      cp_async_commit();
+      if (l >= 2) {
+        asm volatile("cp.async.wait_group 2;" ::: "memory");
+        fence_proxy_async();
+        mbar_arrive(&bfull[(l - 2) % NST]);
+      }
+    }
+    cp_async_wait_all();
+    fence_proxy_async();
+    for (int l = n > 2 ? n - 2 : 0; l < n; ++l) mbar_arrive(&bfull[l % NST]);
+  } else {
+    // epilogue (warps 8-11): thread = row; tot[b] = sum over the split's groups of s_g D_g
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int64_t grow = (int64_t)rb * kRowBlock + r;
+    float tot[NT];
+#pragma unroll
+    for (int b = 0; b < NT; ++b) tot[b] = 0.f;
+    int gcount = 0;
+    for (int l = 0; l < n; ++l) {
+      const bool last = l == n - 1 || grp(l) != grp(l + 1);
+      if (!last) continue;
+      const int gi = grp(l);
+      const int buf = grouped ? gcount % NDB : 0;
+      const uint32_t szw = __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off +
+                                                                    ((int64_t)rb * g.G + gi) * kSZBlockBytes) + r);
+      const float sc = __low2float(*reinterpret_cast<const __half2*>(&szw));
+      mbar_wait(&dfull[buf], (uint32_t)(gcount / NDB) & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < NT / 16; ++c) {
+        uint32_t d[16];
+        tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * NT + c * 16), d);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) tot[c * 16 + j] = fmaf(sc, __uint_as_float(d[j]), tot[c * 16 + j]);
+      }
+      tc_fence_before();
+      mbar_arrive(&dempty[buf]);
+      ++gcount;
+    }
+    pdl_wait();   // y, the workspace and x (weak fold) belong to earlier kernels until they complete
+    if (split == 0 && g.k > 0) {   // fp16 weak columns x gathered fp16 x, added once
+      const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
+      const uint8_t* wrec = p.blob + g.units_off + (int64_t)rb * g.rb_bytes + (int64_t)g.nss * g.ss_bytes;
+      for (int tt = 0; tt < g.k; ++tt) {
+        const int ch = tt / kWeakChunk, c = tt % kWeakChunk;
+        const __half wv = ch < g.nfull
+                              ? *reinterpret_cast<const __half*>(wrec + (int64_t)ch * kWeakChunkBytes + (r * kWeakChunk + c) * 2)
+                              : *reinterpret_cast<const __half*>(wrec + (int64_t)g.nfull * kWeakChunkBytes + (r * g.ktail + c) * 2);
+        const float wf = __half2float(wv);
+        const int j = __ldg(widx + tt);
+#pragma unroll
+        for (int b = 0; b < NT; ++b)
+          if (b < p.B) tot[b] = fmaf(wf, __half2float(p.x[(int64_t)b * g.K + j]), tot[b]);
+      }
+    }
+    if (p.KS == 1) {
+      if (grow < g.M)
+#pragma unroll
+        for (int b = 0; b < NT; ++b)
+          if (b < p.B) {
+            if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = tot[b];
+            else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(tot[b]);
+          }
+    } else {
+      const int64_t Mp = (int64_t)g.nrb * kRowBlock;
+#pragma unroll
+      for (int b = 0; b < NT; ++b)
+        if (b < p.B) __stcg(&p.part[((int64_t)split * p.B + b) * Mp + grow], tot[b]);
+      named_sync(1, 128);
+      if (r == 0) {
+        unsigned old;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(p.counters + rb) : "memory");
+        const int lastc = old == (unsigned)(p.KS - 1);
+        if (lastc) p.counters[rb] = 0u;
+        *flag = lastc;
+      }
+      named_sync(1, 128);
+      if (*flag && grow < g.M) {
+        for (int b = 0; b < p.B; ++b) {
+          float v = 0.f;
+          for (int sp = 0; sp < p.KS; ++sp) v += __ldcg(&p.part[((int64_t)sp * p.B + b) * Mp + grow]);
+          if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = v;
+          else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(v);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kProd) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  }
+}
+
+// splits of K (in super-steps, on group boundaries) so that the grid covers the SMs ~2x
+static void plan(const Geo& g, int sms, int& KS, int& sps, int& gss) {
+  gss = g.group ? g.group / 64 : 0;
+  const int unit = gss ? gss : SUB;
+  const int units = (g.nss + unit - 1) / unit;
+  int want = std::max(1, (2 * sms + g.nrb - 1) / g.nrb);
+  want = std::min(want, units);
+  const int upc = (units + want - 1) / want;   // units per split
+  sps = upc * unit;
+  KS = (g.nss + sps - 1) / sps;
+}
+
+size_t workspace_bytes(const Geo& g, int B, int sms) {
+  int KS, sps, gss;
+  plan(g, sms, KS, sps, gss);
+  return (size_t)g.nrb * 4 + 256 + (KS > 1 ? (size_t)KS * B * g.nrb * kRowBlock * 4 : 0);
+}
+
+template <int BITS, int NT>
+static owq_status launch_t(Params& p, cudaStream_t stream) {
+  auto kern = owq_gemm_sb_kernel<BITS, NT>;
+  const uint32_t smem = NST * stage_bytes<NT>() + 1024 + 512;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool configured[16] = {};
+  if (!configured[dev & 15]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return OWQ_ERR_CUDA;
+    configured[dev & 15] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)p.KS, (unsigned)p.g.nrb);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, p);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "owq: launch of owq_gemm_sb_kernel failed: %s\n", cudaGetErrorString(e));
+    return OWQ_ERR_CUDA;
+  }
+  return OWQ_OK;
+}
+
+owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, void* ws,
+                  size_t ws_bytes, int sms, cudaStream_t stream) {
+  if (B < 1 || B > 32) return OWQ_ERR_UNSUPPORTED;
+  if (g.group && (g.group % (64 * SUB))) return OWQ_ERR_UNSUPPORTED;   // stages never straddle a scale group
+  if (ws_bytes < workspace_bytes(g, B, sms)) return OWQ_ERR_BUFFER_TOO_SMALL;
+  Params p{};
+  p.blob = (const uint8_t*)blob;
+  p.x = (const __half*)x;
+  p.y = y;
+  p.counters = (uint32_t*)ws;
+  p.part = (float*)((uint8_t*)ws + ((size_t)g.nrb * 4 + 255) / 256 * 256);
+  p.g = g;
+  p.B = B;
+  p.y_f32 = y_f32 ? 1 : 0;
+  plan(g, sms, p.KS, p.sps, p.gss);
+  if (g.bits == 3) return B <= 16 ? launch_t<3, 16>(p, stream) : launch_t<3, 32>(p, stream);
+  return B <= 16 ? launch_t<4, 16>(p, stream) : launch_t<4, 32>(p, stream);
+}
+
+}  // namespace sb
 }  // namespace pf
 }  // namespace owq
