@@ -261,6 +261,10 @@ typedef struct owq_tp owq_tp;   /* owns one ncclComm_t */
 owq_status owq_tp_get_unique_id(void *id128);
 owq_status owq_tp_init(const void *id128, int world, int rank, owq_tp **out);
 owq_status owq_tp_destroy(owq_tp *tp);
+/* Host poll of the communicator's asynchronous error state
+ * (ncclCommGetAsyncError): OWQ_OK, or OWQ_ERR_NCCL once a collective enqueued by
+ * owq_tp_gemv has failed (a peer died, a network error).  Non-blocking. */
+owq_status owq_tp_check(owq_tp *tp);
 
 /* Slice of `full` owned by `rank` (host only, no GPU needed).  ROWS: rows
  * [r0, r1) with r0 = round(rank*M/world) to a multiple of 16; every column,

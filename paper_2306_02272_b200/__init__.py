@@ -28,7 +28,8 @@ __all__ = [
     "OWQ_PACK_U8_CODES", "OWQ_PACK_LAYOUT_CC", "OWQ_LAYOUT_TC", "OWQ_LAYOUT_CC",
     "owq_packed_bytes_layout", "owq_workspace_bytes_grid", "owq_packed_bytes_colmap", "owq_pack_host_colmap",
     "owq_pack_colmap", "owq_blob_colmap_host", "choose_layout", "owq_quantize_gpu",
-    "owq_quantize_workspace_bytes", "owq_gemm_prefill", "owq_gemm_batch_f16", "EXPORTED_SYMBOLS",
+    "owq_quantize_workspace_bytes", "owq_gemm_prefill", "owq_gemm_batch_f16", "owq_tp_check",
+    "EXPORTED_SYMBOLS",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -47,6 +48,7 @@ EXPORTED_SYMBOLS = [
     "owq_tp_gemv", "owq_tp_bounds", "owq_status_string", "owq_packed_bytes_colmap",
     "owq_pack_host_colmap", "owq_pack_colmap", "owq_blob_colmap_host",
     "owq_quantize_workspace_bytes", "owq_quantize_gpu", "owq_gemm_prefill", "owq_gemm_batch_f16",
+    "owq_tp_check",
 ]
 
 
@@ -112,6 +114,7 @@ def lib():
         "owq_tp_get_unique_id": (st, [_P]),
         "owq_tp_init": (st, [_P, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
         "owq_tp_destroy": (st, [_P]),
+        "owq_tp_check": (st, [_P]),
         "owq_tp_bounds": (st, [_S, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]),
         "owq_tp_shard_shape": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.c_int, ctypes.c_int,
@@ -467,6 +470,11 @@ def owq_tp_init(uid: bytes, world: int, rank: int):
     h = ctypes.c_void_p()
     _check(lib().owq_tp_init(ctypes.cast(buf, ctypes.c_void_p), world, rank, ctypes.byref(h)))
     return h
+
+
+def owq_tp_check(h):
+    """Raise OwqError if an NCCL collective of this communicator failed (non-blocking poll)."""
+    _check(lib().owq_tp_check(h))
 
 
 def owq_tp_destroy(h):

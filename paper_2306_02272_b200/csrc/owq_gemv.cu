@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -1175,40 +1176,56 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
         // weak chunks (straight from the blob, not through the ring): fp16 weak
         // columns x gathered activations, fp32 (unscaled)
         const uint8_t* wbase = p.blob + g.units_off + item_offset(g, crb, cli);
-        for (int pi = 0; pi < cn; ++pi) {
-          const int gch = cli - g.nss + pi;
-          float v[8];
-          if (gch < g.nfull) {
-            const int64_t w0 = (i0 > crb * n_rb + g.nss ? i0 - crb * n_rb : g.nss) - g.nss;
-            const int jpre = (int)(gch - w0);
-            const uint4 a = (wpre_rb == crb && jpre >= 0 && jpre < 2)
-                                ? (jpre == 0 ? wpre[0] : wpre[1])
-                                : __ldg(reinterpret_cast<const uint4*>(wbase + (size_t)pi * kWeakChunkBytes + row * 16));
-            const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
+        const int64_t w0 = (i0 > crb * n_rb + g.nss ? i0 - crb * n_rb : g.nss) - g.nss;
+        // four chunk loads in flight per batch (k = 153 has 20 chunks per row-block;
+        // one load at a time left the epilogue latency-bound, DESIGN.md §6.2 k-sweep)
+        for (int pi0 = 0; pi0 < cn; pi0 += 4) {
+          uint4 av[4];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              const float2 f = __half22float2(u2h(aw[c]));
-              v[2 * c] = f.x;
-              v[2 * c + 1] = f.y;
+          for (int u = 0; u < 4; ++u) {
+            const int pi = pi0 + u;
+            const int gch = cli - g.nss + pi;
+            av[u] = make_uint4(0, 0, 0, 0);
+            if (pi < cn && gch < g.nfull) {
+              const int jpre = (int)(gch - w0);
+              av[u] = (wpre_rb == crb && jpre >= 0 && jpre < 2)
+                          ? (jpre == 0 ? wpre[0] : wpre[1])
+                          : __ldg(reinterpret_cast<const uint4*>(wbase + (size_t)pi * kWeakChunkBytes + row * 16));
             }
-          } else {
-            const __half* tl = reinterpret_cast<const __half*>(wbase + (size_t)pi * kWeakChunkBytes);
-#pragma unroll
-            for (int c = 0; c < 8; ++c) v[c] = c < g.ktail ? __half2float(tl[row * g.ktail + c]) : 0.f;
           }
 #pragma unroll
-          for (int b = 0; b < MAXB; ++b) {
-            if (b < p.B) {
-              const uint4 xv = *reinterpret_cast<const uint4*>(xw + b * g.kpad + gch * kWeakChunk);
-              const uint32_t xwv[4] = {xv.x, xv.y, xv.z, xv.w};
-              float acc = tot[b];
+          for (int u = 0; u < 4; ++u) {
+            const int pi = pi0 + u;
+            if (pi >= cn) break;
+            const int gch = cli - g.nss + pi;
+            float v[8];
+            if (gch < g.nfull) {
+              const uint32_t aw[4] = {av[u].x, av[u].y, av[u].z, av[u].w};
 #pragma unroll
               for (int c = 0; c < 4; ++c) {
-                const float2 f = __half22float2(u2h(xwv[c]));
-                acc = fmaf(v[2 * c], f.x, acc);
-                acc = fmaf(v[2 * c + 1], f.y, acc);
+                const float2 f = __half22float2(u2h(aw[c]));
+                v[2 * c] = f.x;
+                v[2 * c + 1] = f.y;
               }
-              tot[b] = acc;
+            } else {
+              const __half* tl = reinterpret_cast<const __half*>(wbase + (size_t)pi * kWeakChunkBytes);
+#pragma unroll
+              for (int c = 0; c < 8; ++c) v[c] = c < g.ktail ? __half2float(tl[row * g.ktail + c]) : 0.f;
+            }
+#pragma unroll
+            for (int b = 0; b < MAXB; ++b) {
+              if (b < p.B) {
+                const uint4 xv = *reinterpret_cast<const uint4*>(xw + b * g.kpad + gch * kWeakChunk);
+                const uint32_t xwv[4] = {xv.x, xv.y, xv.z, xv.w};
+                float acc = tot[b];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  const float2 f = __half22float2(u2h(xwv[c]));
+                  acc = fmaf(v[2 * c], f.x, acc);
+                  acc = fmaf(v[2 * c + 1], f.y, acc);
+                }
+                tot[b] = acc;
+              }
             }
           }
         }
@@ -1496,11 +1513,13 @@ static owq_status launch(const Params& p0, int64_t grid, cudaStream_t stream) {
   p.nst = nst;
   const size_t smem = (size_t)nst * p.stage_bytes + fixed + (size_t)nst * 32;
   auto kern = owq_gemv_kernel<BITS, NN, DWG, GRP>;
-  static thread_local size_t configured = 0;
-  if (configured < smem) {
+  // the attribute is per device: one record per device, atomically raised
+  static std::atomic<size_t> configured[32];
+  if (configured[dev & 31].load() < smem) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return OWQ_ERR_CUDA;
-    configured = smem;
+    size_t cur = configured[dev & 31].load();
+    while (cur < smem && !configured[dev & 31].compare_exchange_weak(cur, smem)) {}
   }
   static const int pdl = knob("OWQ_PDL", 2);   // 0 off, 1 GEMV, 2 both
   cudaLaunchConfig_t cfg = {};
@@ -1744,10 +1763,11 @@ size_t owq_workspace_bytes_grid(const owq_shape* s, int batch, int grid) {
   const Geo g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
   // an upper bound for any n_weak: the requested grid before the per-shape cap
   const int64_t G = grid > 0 ? grid : device_sms();
-  if (G > kMaxGrid) return 0;
+  if (G > 1024) return 0;   // the CUDA-core kernel's limit (the tcgen05 kernel's is 512)
   // one workspace serves either layout of the layer and the small-batch f16 kernel
   const size_t sbw = ws_sync() + pf::sb::workspace_bytes(g, 32, device_sms());   // any batch <= 32
-  return std::max(std::max(ws_bytes_for(g, batch, G), cc::workspace_bytes((int)G, std::min(batch, 4))), sbw);
+  const size_t v3 = G <= kMaxGrid ? ws_bytes_for(g, batch, G) : 0;
+  return std::max(std::max(v3, cc::workspace_bytes((int)G, std::min(batch, 4))), sbw);
 }
 
 size_t owq_workspace_bytes(const owq_shape* s, int batch) { return owq_workspace_bytes_grid(s, batch, 0); }

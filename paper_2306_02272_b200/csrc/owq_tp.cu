@@ -86,6 +86,13 @@ owq_status owq_tp_init(const void* id128, int world, int rank, owq_tp** out) {
   return OWQ_OK;
 }
 
+owq_status owq_tp_check(owq_tp* tp) {
+  if (!tp) return OWQ_ERR_INVALID_ARG;
+  ncclResult_t async = ncclSuccess;
+  if (ncclCommGetAsyncError(tp->comm, &async) != ncclSuccess) return OWQ_ERR_NCCL;
+  return async == ncclSuccess || async == ncclInProgress ? OWQ_OK : OWQ_ERR_NCCL;
+}
+
 owq_status owq_tp_destroy(owq_tp* tp) {
   if (!tp) return OWQ_ERR_INVALID_ARG;
   ncclResult_t r = ncclCommDestroy(tp->comm);
