@@ -1432,7 +1432,7 @@ static owq_status blob_layout(const owq_shape* s, const void* d_packed, cudaStre
     auto it = g_reg.find(RegKey{d_packed, *s});
     if (it != g_reg.end()) { layout = it->second.layout; Ks = it->second.Ks; return OWQ_OK; }
   }
-  uint8_t hb[64];
+  uint8_t hb[128];   // >= sizeof either header struct
   if (cudaMemcpyAsync(hb, d_packed, sizeof(hb), cudaMemcpyDeviceToHost, stream) != cudaSuccess ||
       cudaStreamSynchronize(stream) != cudaSuccess)
     return OWQ_ERR_CUDA;
