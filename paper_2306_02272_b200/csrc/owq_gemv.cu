@@ -891,6 +891,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
     constexpr double kPow256[6] = {1.0, 256.0, 65536.0, 16777216.0, 4294967296.0, 1099511627776.0};
     const int gl = g.group ? p.group_log2 : 30;
     float tot[MAXB];
+    float keep[MAXB];                                    // summed row-block held back to the end (fixup)
+    int64_t keep_rb = -1;
     long long sacc[MAXB];                                // this thread's share of the open group's digit sums
 #pragma unroll
     for (int b = 0; b < MAXB; ++b) { tot[b] = 0.f; sacc[b] = 0; }
@@ -1256,43 +1258,23 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           const int npieces = (int)(c_last - c_first + 1);
           uint32_t* pw = p.slots;   // [cta][B][128]: each CTA has at most one non-summer piece (its first row-block)
           if (p.coresident) {
-            // Fixed summer = the CTA holding the row-block's first item (it reaches
-            // the row-block last).  The other pieces store their partial rows as
-            // ~bits (a zero word = not written yet: the workspace starts zeroed and
-            // the summer zeroes what it consumed), so each summer thread polls its
-            // own rows' words -- no fences, counters or barriers -- and adds the
-            // pieces in a fixed order.
-            if (cta != c_first) {
+            // Fixed summer = the CTA holding the row-block's LAST item (the
+            // highest-index piece, CUTLASS's stream-K rule).  For that CTA the
+            // row-block is its first one, so it keeps its partial in registers and
+            // sums after all its own work; every other piece is its CTA's last
+            // row-block and is stored (as ~bits: a zero word = not written yet; the
+            // workspace starts zeroed and the summer zeroes what it consumed)
+            // before that CTA waits on anything.  A summer only ever waits on
+            // lower-index CTAs, so progress needs in-order dispatch, not
+            // co-residency of the whole grid.
+            if (cta != c_last) {
 #pragma unroll
               for (int b = 0; b < MAXB; ++b)
                 if (b < p.B) st_relaxed(pw + (cta * p.B + b) * kRowBlock + row, ~__float_as_uint(tot[b]));
             } else {
-              for (int qq = 1; qq < npieces; ++qq) {
-                // all batch rows of piece qq in flight at once, then wait for the late ones
-                uint32_t w[MAXB];
 #pragma unroll
-                for (int b = 0; b < MAXB; ++b)
-                  w[b] = b < p.B ? ld_relaxed(pw + ((c_first + qq) * p.B + b) * kRowBlock + row) : 1u;
-#pragma unroll
-                for (int b = 0; b < MAXB; ++b)
-                  if (b < p.B) {
-                    uint32_t* a = pw + ((c_first + qq) * p.B + b) * kRowBlock + row;
-                    while (w[b] == 0u) {
-                      __nanosleep(32);
-                      w[b] = ld_relaxed(a);
-                    }
-                    st_relaxed(a, 0u);
-                    tot[b] += __uint_as_float(~w[b]);
-                  }
-              }
-              if (grow < g.M) {
-#pragma unroll
-                for (int b = 0; b < MAXB; ++b)
-                  if (b < p.B) {
-                    if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = tot[b];
-                    else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(tot[b]);
-                  }
-              }
+              for (int b = 0; b < MAXB; ++b) keep[b] = tot[b];
+              keep_rb = crb;
             }
           } else {
             // grids larger than the SM count: the last piece to arrive sums (acq_rel
@@ -1333,6 +1315,42 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       crb = nrb;
       cli = nli;
       cn = nn;
+    }
+    if (keep_rb >= 0) {
+      // summer of its first row-block: add the lower pieces in CTA order, then its own
+      int64_t c_first, c_last;
+      pieces(keep_rb, c_first, c_last);
+      uint32_t* pw = p.slots;
+      float v[MAXB];
+#pragma unroll
+      for (int b = 0; b < MAXB; ++b) v[b] = 0.f;
+      for (int64_t c = c_first; c < c_last; ++c) {
+        // all batch rows of piece c in flight at once, then wait for the late ones
+        uint32_t w[MAXB];
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) w[b] = b < p.B ? ld_relaxed(pw + (c * p.B + b) * kRowBlock + row) : 1u;
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b)
+          if (b < p.B) {
+            uint32_t* a = pw + (c * p.B + b) * kRowBlock + row;
+            while (w[b] == 0u) {
+              __nanosleep(32);
+              w[b] = ld_relaxed(a);
+            }
+            st_relaxed(a, 0u);
+            v[b] += __uint_as_float(~w[b]);
+          }
+      }
+      const int64_t grow = keep_rb * kRowBlock + row;
+      if (grow < g.M) {
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b)
+          if (b < p.B) {
+            const float r = v[b] + keep[b];
+            if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = r;
+            else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(r);
+          }
+      }
     }
     if (kTrace && p.trace && et == 0) {
       p.trace[cta * 256 + 53] = (unsigned long long)e_ring;

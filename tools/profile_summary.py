@@ -25,6 +25,8 @@ SHAPES = {
     "qkv": (3 * 12288, 12288, 3, 0, 15, 1),
     "b8": (12288, 12288, 3, 0, 15, 8), "b16": (12288, 12288, 3, 0, 15, 16),
     "g128": (12288, 12288, 4, 128, 15, 1), "llama_up_b8": (11008, 4096, 4, 128, 1, 8),
+    "cc_q": (12288, 12288, 3, 0, 15, 1), "cc_g128": (12288, 12288, 4, 128, 15, 1),
+    "sb_llama_up_b8": (11008, 4096, 4, 128, 1, 8), "prefill": (12288, 12288, 3, 0, 15, 2048),
 }
 
 
@@ -54,18 +56,18 @@ def main(rnd):
             out.append(f"| `{k}` | {len(v)} | {sorted(v)[len(v) // 2] * 1e6:.2f} | {sum(v) / tot * 100:.1f}% |")
     traffic = {}
     out.append("\n## `ncu --set full` of one GEMV launch per shape\n")
-    out.append("| shape | B | duration us | DRAM read MB | DRAM write MB | algorithmic MB | read / alg | "
+    out.append("| shape | kernel | B | duration us | DRAM read MB | DRAM write MB | algorithmic MB | read / alg | "
                "ALU % | FMA % | tensor-mem active % | issue % | SM MHz |")
-    out.append("|---|---|---|---|---|---|---|---|---|---|---|---|")
+    out.append("|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for tag, shp in SHAPES.items():
         rep = os.path.join(P, f"prof_{rnd}_{tag}.ncu-rep")
         if not os.path.exists(rep):
             continue
         L = ncu_csv.launches(rep, "owq_")
-        L = [x for x in L if "gemv" in str(x.get("Kernel Name", x.get("Function Name", "gemv")))] or L
         if not L:
             continue
         g = L[0]
+        kname = str(g.get("Kernel Name", g.get("Function Name", "?"))).split("(")[0].split("<")[0]
         alg = algorithmic_bytes(*shp)
         rd, wr = g["dram__bytes_read.sum"], g["dram__bytes_write.sum"]
         dur = g["gpu__time_duration.sum"]
@@ -77,7 +79,7 @@ def main(rnd):
         tc = "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active"
         traffic[tag] = {"dram_read_bytes": rd, "dram_write_bytes": wr, "algorithmic_bytes": alg,
                         "duration_us": dur * 1e6, "batch": shp[5]}
-        out.append(f"| {tag} {shp[0]}x{shp[1]} b{shp[2]} g{shp[3]} k{shp[4]} | {shp[5]} | {dur * 1e6:.2f} | "
+        out.append(f"| {tag} {shp[0]}x{shp[1]} b{shp[2]} g{shp[3]} k{shp[4]} | `{kname}` | {shp[5]} | {dur * 1e6:.2f} | "
                    f"{rd / 1e6:.3f} | {wr / 1e6:.4f} | {alg / 1e6:.3f} | {rd / alg:.4f} | "
                    f"{pct('sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active')} | "
                    f"{pct('sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active')} | "
