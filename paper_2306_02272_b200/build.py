@@ -52,6 +52,8 @@ def build(force: bool = False, verbose: bool = False, csrc: str = None, out: str
     """csrc/out/inc/defines: experiments only (A/B builds of another source tree or
     with -D knobs into another file; the product build uses the defaults)."""
     global CSRC, OUT, BUILD, INC
+    if defines and not out:
+        raise ValueError("-D builds are experiments: give --out (the product library is built without them)")
     if csrc or out or inc or defines:
         CSRC, OUT, INC = csrc or CSRC, out or OUT, inc or INC
         BUILD = OUT + "_build"

@@ -891,8 +891,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
     constexpr double kPow256[6] = {1.0, 256.0, 65536.0, 16777216.0, 4294967296.0, 1099511627776.0};
     const int gl = g.group ? p.group_log2 : 30;
     float tot[MAXB];
-    float keep[MAXB];                                    // summed row-block held back to the end (fixup)
-    int64_t keep_rb = -1;
+    int64_t keep_rb = -1;                                // row-block this CTA sums at its end (fixup)
     long long sacc[MAXB];                                // this thread's share of the open group's digit sums
 #pragma unroll
     for (int b = 0; b < MAXB; ++b) { tot[b] = 0.f; sacc[b] = 0; }
@@ -1260,8 +1259,10 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           if (p.coresident) {
             // Fixed summer = the CTA holding the row-block's LAST item (the
             // highest-index piece, CUTLASS's stream-K rule).  For that CTA the
-            // row-block is its first one, so it keeps its partial in registers and
-            // sums after all its own work; every other piece is its CTA's last
+            // row-block is its first one, so it parks its partial in its own
+            // partial-row slot (same thread stores and reloads it; registers
+            // live across the whole loop spilled the batch variants) and sums
+            // after all its own work; every other piece is its CTA's last
             // row-block and is stored (as ~bits: a zero word = not written yet; the
             // workspace starts zeroed and the summer zeroes what it consumed)
             // before that CTA waits on anything.  A summer only ever waits on
@@ -1273,7 +1274,8 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
                 if (b < p.B) st_relaxed(pw + (cta * p.B + b) * kRowBlock + row, ~__float_as_uint(tot[b]));
             } else {
 #pragma unroll
-              for (int b = 0; b < MAXB; ++b) keep[b] = tot[b];
+              for (int b = 0; b < MAXB; ++b)
+                if (b < p.B) p.partial[(cta * p.B + b) * kRowBlock + row] = tot[b];
               keep_rb = crb;
             }
           } else {
@@ -1346,7 +1348,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
 #pragma unroll
         for (int b = 0; b < MAXB; ++b)
           if (b < p.B) {
-            const float r = v[b] + keep[b];
+            const float r = v[b] + p.partial[(cta * p.B + b) * kRowBlock + row];
             if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = r;
             else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(r);
           }

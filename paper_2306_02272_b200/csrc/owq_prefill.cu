@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
       const uint32_t ph = (uint32_t)(ss / NST) & 1u;
       mbar_wait(&afull[s], ph);
       mbar_wait(&bfull[s], ph);
+      fence_proxy_async();   // the landed cp.async (generic-proxy) writes, before the MMA's async-proxy reads
       tc_fence_after();
       if (lane == 0) {
         const uint32_t b0 = smem_u32(Bt(s));
@@ -254,7 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
     }
     }
   } else if (warp < kProdW) {
-    // ------------------------------------------------ x loaders: cp.async, NST - 1 stages in flight
+    // ------------------------------------------------ x loaders: cp.async, up to NST stages in flight;
+    // each lane's copies of a stage arrive on bfull when they land (round 2 published
+    // stage ss - 1 after a cp.async.wait_group at stage ss: one stage of lookahead)
     const int t = threadIdx.x - kDecW * 32;
     constexpr int LT = kLoadW * 32;
     const int64_t tok0 = (int64_t)tile * NT;
@@ -271,16 +274,9 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
         const __half* src = ok ? p.x + (tok0 + n) * g.K + col : p.x;
         cp_async16(b0 + (uint32_t)kc * (NT * 16) + (uint32_t)(n >> 3) * 128u + (uint32_t)(n & 7) * 16u, src, ok ? 16u : 0u);
       }
-      cp_async_commit();
-      if (ss >= NST - 2) {   // the group of stage ss - (NST - 2) has landed: publish it
-        asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory");
-        fence_proxy_async();
-        mbar_arrive(&bfull[(ss - (NST - 2)) % NST]);
-      }
+      cp_async_arrive_noinc(&bfull[s]);
     }
     cp_async_wait_all();
-    fence_proxy_async();
-    for (int ss = (nss > NST - 2 ? nss - (NST - 2) : 0); ss < nss; ++ss) mbar_arrive(&bfull[ss % NST]);
   }
 done:
   tc_fence_before();
@@ -341,7 +337,28 @@ owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void
 // ============================================================================
 namespace sb {
 
-constexpr int NST = 4;
+#ifdef OWQ_EXPERIMENTS
+// per-stage clock64 stamps of CTA (0, 0): [event][stage], events 0 producer after
+// empty, 1 decode after full, 2 decode arrive afull, 3 MMA after afull, 4 MMA after
+// bfull, 5 loader after empty, 6 loader arrive, 7 epilogue after dfull
+__device__ long long g_sb_trace[8][64];
+__device__ unsigned long long g_sb_cta[3][1024];   // per CTA: globaltimer at start, after the loader's pdl_wait, at exit
+__device__ __forceinline__ unsigned long long sb_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SB_CTA(ev) do { const int c_ = blockIdx.y * gridDim.x + blockIdx.x; if (c_ < 1024) g_sb_cta[ev][c_] = sb_gtime(); } while (0)
+#define SB_TR(ev, l) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (l) < 64) g_sb_trace[ev][l] = clock64(); } while (0)
+#else
+#define SB_TR(ev, l) do { } while (0)
+#define SB_CTA(ev) do { } while (0)
+#endif
+
+#ifndef OWQ_SB_NST
+#define OWQ_SB_NST 4
+#endif
+constexpr int NST = OWQ_SB_NST;
 #ifndef OWQ_SB_SUB
 #define OWQ_SB_SUB 1
 #endif
@@ -351,7 +368,12 @@ constexpr int NST = 4;
 constexpr int SUB = OWQ_SB_SUB;
 constexpr uint32_t A_BYTES = 128 * 64 * 2;
 constexpr uint32_t C_MAX = 128 * 8 * 4;
-constexpr int NDB = 4;                  // D buffers (grouped scales)
+constexpr int NDB = 4;                  // D buffers (one per drain in flight)
+// Per-row scales: D is still drained into fp32 registers every kDrainSS
+// super-steps.  One TMEM accumulator over all of K = 12288 (one split) lost
+// precision (B = 32 parity error 4.8e-3 > the 2e-3 bound): one fp32 TMEM
+// accumulator over a chain of 768 MMAs.
+constexpr int kDrainSS = 8;
 // warps: 0-7 decode (4 per sub-step, thread = row), 8-11 epilogue, 12 x loader, 13 producer, 14 MMA
 constexpr int kDec = 4 * SUB, kEpi0 = kDec, kLoad = kEpi0 + 4, kProd = kLoad + 1, kMma = kProd + 1;
 constexpr int kThreads = (kMma + 1) * 32;
@@ -364,7 +386,9 @@ struct Params {
   uint32_t* counters;   // [nrb], zero between calls
   Geo g;
   int32_t B, y_f32, KS, sps;   // splits, super-steps per split (a multiple of SUB)
-  int32_t gss;          // super-steps per scale group (0 = per-row scales; else a multiple of SUB)
+  int32_t gss;          // super-steps per D drain: the scale group, or kDrainSS with per-row scales
+  int32_t skip;         // experiment builds only (OWQ_SB_SKIP): 1 decode, 2 MMA, 4 x copies, 8 code copies,
+                        // 16 MMA-side proxy fence, 32 commits -> plain arrives (with 2)
 };
 
 template <int NT>
@@ -392,12 +416,13 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
   auto A = [&](int s, int u) { return base + (size_t)s * STG + (size_t)u * A_BYTES; };
   auto Bt = [&](int s, int u) { return base + (size_t)s * STG + SUB * A_BYTES + (size_t)u * (NT * 128); };
   auto Cd = [&](int s) { return base + (size_t)s * STG + SUB * (A_BYTES + NT * 128); };
-  const bool grouped = p.gss > 0;
+  const bool grouped = g.group != 0;   // per-group scales (else per row: one (s, z) per row)
+  if (threadIdx.x == 0) SB_CTA(0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&afull[s], kDec * 32);
-      mbar_init(&bfull[s], 32);
+      mbar_init(&afull[s], kDec * 32 + 32);   // decode threads + the loader lanes' cp.async arrivals
+      mbar_init(&bfull[s], 1);                 // (unused)
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < NDB; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], 128); }
@@ -413,7 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
   const uint32_t tmem = *tslot;
   const uint32_t ssb = (uint32_t)g.ss_bytes;
   // scale group of stage l (stages never straddle a group: gss is a multiple of SUB)
-  auto grp = [&](int l) { return grouped ? (ss0 + SUB * l) / p.gss : 0; };
+  auto grp = [&](int l) { return (ss0 + SUB * l) / p.gss; };   // D drain (= scale group when grouped)
+  auto sgrp = [&](int l) { return grouped ? grp(l) : 0; };      // (s, z) block
   auto nsub = [&](int l) { return min(SUB, nsteps - SUB * l); };
 
   if (warp == kProd) {
@@ -422,7 +448,12 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
       for (int l = 0; l < n; ++l) {
         const int s = l % NST;
         if (l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
+        SB_TR(0, l);
         const uint32_t bytes = ssb * (uint32_t)nsub(l);   // consecutive super-steps are contiguous in the blob
+        if (p.skip & 8) {
+          mbar_arrive(&full[s]);
+          continue;
+        }
         mbar_expect_tx(&full[s], bytes);
         bulk_g2s(Cd(s), p.blob + g.units_off + item_offset(g, rb, ss0 + SUB * l), bytes, &full[s]);
       }
@@ -430,27 +461,35 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
   } else if (warp == kMma) {
     constexpr uint32_t idesc = idesc_f16(128, NT);
     int gcount = 0;
+    int gpos = 0;   // super-steps into the current drain group (splits start on group boundaries)
     for (int l = 0; l < n; ++l) {
       const int s = l % NST;
       const uint32_t ph = (uint32_t)(l / NST) & 1u;
-      const bool first = l == 0 || grp(l) != grp(l - 1);
-      const bool last = l == n - 1 || grp(l) != grp(l + 1);
-      const int buf = grouped ? gcount % NDB : 0;
-      if (first && grouped && gcount >= NDB) mbar_wait(&dempty[buf], (uint32_t)((gcount / NDB) - 1) & 1u);
-      mbar_wait(&afull[s], ph);
-      mbar_wait(&bfull[s], ph);
+      const bool first = gpos == 0;
+      gpos += SUB;
+      const bool last = l == n - 1 || gpos == p.gss;
+      if (gpos == p.gss) gpos = 0;
+      const int buf = gcount % NDB;
+      // one lane waits (parked waiters on a barrier cost every phase change)
+      if (lane == 0 && first && gcount >= NDB) mbar_wait(&dempty[buf], (uint32_t)((gcount / NDB) - 1) & 1u);
+      if (lane == 0) mbar_wait(&afull[s], ph);   // A decoded and the x tile landed
+      if (lane == 0) SB_TR(3, l);
+      if (lane == 0) SB_TR(4, l);
+      if (!(p.skip & 16)) fence_proxy_async();   // the landed cp.async (generic-proxy) writes, before the MMA's async-proxy reads
       tc_fence_after();
       if (lane == 0) {
-        const int nu = nsub(l);
-        for (int u = 0; u < nu; ++u) {
-          const uint32_t a0 = smem_u32(A(s, u)), b0 = smem_u32(Bt(s, u));
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            tc_mma_f16_ss(tmem + (uint32_t)(buf * NT), umma_desc(a0 + kk * 2 * 2048, 2048, 128),
-                          umma_desc(b0 + kk * 2 * (NT * 16), NT * 16, 128), idesc, (first && u == 0 && kk == 0) ? 0u : 1u);
+        const int nu = (p.skip & 2) ? 0 : nsub(l);
+        for (int u = 0; u < nu; ++u)
+          tc_mma_f16_ss_k64<2 * 2048, 2 * NT * 16>(tmem + (uint32_t)(buf * NT), umma_desc(smem_u32(A(s, u)), 2048, 128),
+                                                   umma_desc(smem_u32(Bt(s, u)), NT * 16, 128), idesc,
+                                                   (first && u == 0) ? 0u : 1u);
+        if (p.skip & 32) {
+          mbar_arrive(&empty[s]);
+          if (last) mbar_arrive(&dfull[buf]);
+        } else {
+          tc_commit(&empty[s]);
+          if (last) tc_commit(&dfull[buf]);
         }
-        tc_commit(&empty[s]);
-        if (last) tc_commit(&dfull[buf]);
       }
       __syncwarp();
       if (last) ++gcount;
@@ -460,20 +499,34 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
     const int u = warp >> 2;
     const int r = (warp & 3) * 32 + lane;
     constexpr int WPR = BITS == 3 ? 6 : 8;
+    // the row's (scale, zero) words of the split's groups, loaded two groups
+    // ahead (one load per group in the stage loop left every group start waiting
+    // on a global load, ~9 % of the stall samples at g128)
+    auto ldsz = [&](int gi) {
+      return gi < g.G ? __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off + ((int64_t)rb * g.G + gi) * kSZBlockBytes) + r)
+                      : 0u;
+    };
+    const int gfirst = sgrp(0);
+    uint32_t sz0 = ldsz(gfirst), sz1 = grouped ? ldsz(gfirst + 1) : 0u, sz2 = grouped ? ldsz(gfirst + 2) : 0u;
     uint32_t zzw = 0;
     int zg = -1;
     for (int l = 0; l < n; ++l) {
       const int s = l % NST;
-      const int gi = grp(l);
+      const int gi = sgrp(l);
       if (gi != zg) {
-        const uint32_t szw = __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off +
-                                                                      ((int64_t)rb * g.G + gi) * kSZBlockBytes) + r);
-        const __half2 zz = __float2half2_rn(1024.f + __high2float(*reinterpret_cast<const __half2*>(&szw)));
+        if (zg >= 0) {   // next group: shift the prefetch window
+          sz0 = sz1;
+          sz1 = sz2;
+          sz2 = ldsz(gi + 2);
+        }
+        const __half2 zz = __float2half2_rn(1024.f + __high2float(*reinterpret_cast<const __half2*>(&sz0)));
         zzw = *reinterpret_cast<const uint32_t*>(&zz);
         zg = gi;
       }
-      mbar_wait(&full[s], (uint32_t)(l / NST) & 1u);
-      if (u < nsub(l)) {
+      if (lane == 0) mbar_wait(&full[s], (uint32_t)(l / NST) & 1u);
+      __syncwarp();
+      if (threadIdx.x == 0) SB_TR(1, l);
+      if (u < nsub(l) && !(p.skip & 1)) {
         const uint8_t* rec = Cd(s) + (size_t)u * ssb;
         uint32_t w[8], o[16];
 #pragma unroll
@@ -494,15 +547,20 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
         fence_proxy_async();
       }
       mbar_arrive(&afull[s]);
+      if (threadIdx.x == 0) SB_TR(2, l);
     }
   } else if (warp == kLoad) {
-    // x loader: NT tokens x (SUB x 64) columns per stage (zero rows past B), 2 stages of lookahead
+    // x loader: NT tokens x (SUB x 64) columns per stage (zero rows past B), up to
+    // NST stages in flight; each lane's copies arrive on afull when they land
     pdl_wait();
+    if (lane == 0) SB_CTA(1);
     for (int l = 0; l < n; ++l) {
       const int s = l % NST;
-      if (l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
+      if (lane == 0 && l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
+      __syncwarp();
+      if (lane == 0) SB_TR(5, l);
 #pragma unroll
-      for (int e = lane; e < SUB * NT * 8; e += 32) {
+      for (int e = lane; e < ((p.skip & 4) ? 0 : SUB * NT * 8); e += 32) {
         const int u = e / (NT * 8), e2 = e % (NT * 8);
         const int t = e2 >> 3, kc = e2 & 7;
         const int64_t col = (int64_t)(ss0 + SUB * l + u) * 64 + kc * 8;
@@ -510,16 +568,10 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
         cp_async16(smem_u32(Bt(s, u)) + (uint32_t)kc * (NT * 16) + (uint32_t)(t >> 3) * 128u + (uint32_t)(t & 7) * 16u,
                    ok ? p.x + (int64_t)t * g.K + col : p.x, ok ? 16u : 0u);
       }
-      cp_async_commit();
-      if (l >= 2) {
-        asm volatile("cp.async.wait_group 2;" ::: "memory");
-        fence_proxy_async();
-        mbar_arrive(&bfull[(l - 2) % NST]);
-      }
+      cp_async_arrive_noinc(&afull[s]);
+      if (lane == 0) SB_TR(6, l);
     }
     cp_async_wait_all();
-    fence_proxy_async();
-    for (int l = n > 2 ? n - 2 : 0; l < n; ++l) mbar_arrive(&bfull[l % NST]);
   } else {
     // epilogue (warps 8-11): thread = row; tot[b] = sum over the split's groups of s_g D_g
     const int q = warp & 3;
@@ -529,15 +581,22 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
 #pragma unroll
     for (int b = 0; b < NT; ++b) tot[b] = 0.f;
     int gcount = 0;
+    auto ldsz = [&](int gi) {
+      return gi < g.G ? __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off + ((int64_t)rb * g.G + gi) * kSZBlockBytes) + r)
+                      : 0u;
+    };
+    uint32_t sznext = ldsz(sgrp(0));   // the next group's (scale, zero), one group ahead
     for (int l = 0; l < n; ++l) {
       const bool last = l == n - 1 || grp(l) != grp(l + 1);
       if (!last) continue;
-      const int gi = grp(l);
-      const int buf = grouped ? gcount % NDB : 0;
-      const uint32_t szw = __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off +
-                                                                    ((int64_t)rb * g.G + gi) * kSZBlockBytes) + r);
+      const int gi = sgrp(l);
+      const int buf = gcount % NDB;
+      const uint32_t szw = sznext;
+      if (grouped) sznext = ldsz(gi + 1);
       const float sc = __low2float(*reinterpret_cast<const __half2*>(&szw));
-      mbar_wait(&dfull[buf], (uint32_t)(gcount / NDB) & 1u);
+      if (lane == 0) mbar_wait(&dfull[buf], (uint32_t)(gcount / NDB) & 1u);
+      __syncwarp();
+      if (r == 0) SB_TR(7, l);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < NT / 16; ++c) {
@@ -604,14 +663,17 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
   }
+  if (threadIdx.x == 0) SB_CTA(2);
 }
 
-// splits of K (in super-steps, on group boundaries) so that the grid covers the SMs ~2x
-static void plan(const Geo& g, int sms, int& KS, int& sps, int& gss) {
-  gss = g.group ? g.group / 64 : 0;
-  const int unit = gss ? gss : SUB;
+// splits of K (in super-steps, on group boundaries): as many as fit one wave of
+// `slots` resident CTAs (round 2 rounded up to 2 x SMs, which left a short
+// second wave -- e.g. 344 CTAs for LLaMA-7B up -- at 1 CTA per SM)
+static void plan(const Geo& g, int slots, int& KS, int& sps, int& gss) {
+  gss = g.group ? g.group / 64 : kDrainSS;
+  const int unit = gss;
   const int units = (g.nss + unit - 1) / unit;
-  int want = std::max(1, (2 * sms + g.nrb - 1) / g.nrb);
+  int want = std::max(1, slots / g.nrb);
   want = std::min(want, units);
   const int upc = (units + want - 1) / want;   // units per split
   sps = upc * unit;
@@ -620,22 +682,42 @@ static void plan(const Geo& g, int sms, int& KS, int& sps, int& gss) {
 
 size_t workspace_bytes(const Geo& g, int B, int sms) {
   int KS, sps, gss;
-  plan(g, sms, KS, sps, gss);
+  plan(g, 2 * sms, KS, sps, gss);   // at most two resident CTAs per SM (launch_t)
   return (size_t)g.nrb * 4 + 256 + (KS > 1 ? (size_t)KS * B * g.nrb * kRowBlock * 4 : 0);
 }
 
 template <int BITS, int NT>
-static owq_status launch_t(Params& p, cudaStream_t stream) {
+static owq_status launch_t(Params& p, int sms, cudaStream_t stream) {
   auto kern = owq_gemm_sb_kernel<BITS, NT>;
   const uint32_t smem = NST * stage_bytes<NT>() + 1024 + 512;
   int dev = 0;
   cudaGetDevice(&dev);
-  static bool configured[16] = {};
-  if (!configured[dev & 15]) {
+  static int occupancy[16] = {};   // resident CTAs per SM (0 = not configured yet)
+  if (!occupancy[dev & 15]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return OWQ_ERR_CUDA;
-    configured[dev & 15] = true;
+    // without a preference the driver picks the smallest carveout that fits ONE
+    // CTA (measured: 1 resident CTA per SM at 92 KB)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
+      return OWQ_ERR_CUDA;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1)
+      return OWQ_ERR_CUDA;
+    occupancy[dev & 15] = std::min(occ, 2);   // workspace_bytes() assumes at most 2
+#ifdef OWQ_EXPERIMENTS
+    {
+      int o0 = 0, o1 = 0, o2 = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, kern, kThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, kern, kThreads, 48 * 1024);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, kern, 32, smem);
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, kern);
+      fprintf(stderr, "owq sb<%d,%d>: %d resident CTAs per SM (smem %u, threads %d); smem 0: %d, 48K: %d, 32 thr: %d; regs %d static %zu maxdyn %d\n",
+              BITS, NT, occ, smem, kThreads, o0, o1, o2, fa.numRegs, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
+    }
+#endif
   }
+  plan(p.g, occupancy[dev & 15] * sms, p.KS, p.sps, p.gss);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -669,11 +751,22 @@ owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void
   p.g = g;
   p.B = B;
   p.y_f32 = y_f32 ? 1 : 0;
-  plan(g, sms, p.KS, p.sps, p.gss);
-  if (g.bits == 3) return B <= 16 ? launch_t<3, 16>(p, stream) : launch_t<3, 32>(p, stream);
-  return B <= 16 ? launch_t<4, 16>(p, stream) : launch_t<4, 32>(p, stream);
+#ifdef OWQ_EXPERIMENTS
+  if (const char* v = getenv("OWQ_SB_SKIP")) p.skip = atoi(v);
+#endif
+  if (g.bits == 3) return B <= 16 ? launch_t<3, 16>(p, sms, stream) : launch_t<3, 32>(p, sms, stream);
+  return B <= 16 ? launch_t<4, 16>(p, sms, stream) : launch_t<4, 32>(p, sms, stream);
 }
 
 }  // namespace sb
 }  // namespace pf
 }  // namespace owq
+
+#ifdef OWQ_EXPERIMENTS
+extern "C" int owq_exp_sb_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, owq::pf::sb::g_sb_trace, sizeof(owq::pf::sb::g_sb_trace));
+}
+extern "C" int owq_exp_sb_cta(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, owq::pf::sb::g_sb_cta, sizeof(owq::pf::sb::g_sb_cta));
+}
+#endif

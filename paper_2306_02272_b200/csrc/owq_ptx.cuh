@@ -39,6 +39,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
+// arrive on `bar` when all of this thread's earlier cp.async copies have landed
+// (.noinc: the arrival is one of the barrier's initial count)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 // make this thread's generic-proxy shared-memory writes visible to the async proxy (tensor core)
@@ -62,6 +67,24 @@ __device__ __forceinline__ void tc_mma_f16_ss(uint32_t d_t, uint64_t a_desc, uin
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_t),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc));
+}
+// Four kind::f16 MMAs (K = 64 in steps of 16) from one thread: operand k-steps
+// are DA / DB bytes apart, i.e. the descriptors' start fields advance by DA/16,
+// DB/16; the first MMA accumulates iff acc != 0, the others always.
+template <uint32_t DA, uint32_t DB>
+__device__ __forceinline__ void tc_mma_f16_ss_k64(uint32_t d_t, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                  uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 a, b;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+      "setp.eq.u32 p, 0, 0;\n\t"
+      "add.u64 a, %1, %5;\n\tadd.u64 b, %2, %6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, p;\n\t"
+      "add.u64 a, a, %5;\n\tadd.u64 b, b, %6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, p;\n\t"
+      "add.u64 a, a, %5;\n\tadd.u64 b, b, %6;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, p;\n\t}" ::"r"(d_t),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(acc), "n"(DA / 16), "n"(DB / 16));
 }
 __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* d) {
   asm volatile(

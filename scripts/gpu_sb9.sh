@@ -1,0 +1,9 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -m paper_2306_02272_b200.build > /dev/null
+python -m paper_2306_02272_b200.build -D OWQ_EXPERIMENTS --out paper_2306_02272_b200/_ab/exp.so > /dev/null
+python -m paper_2306_02272_b200.build -D OWQ_EXPERIMENTS -D OWQ_SB_SUB=2 --out paper_2306_02272_b200/_ab/exp_sub2.so > /dev/null
+(for L in exp exp_sub2; do
+  echo "== $L"; OWQ_LIB=paper_2306_02272_b200/_ab/$L.so timeout 120 python tools/sb_trace.py 12288 12288 3 0 15 8 | sed -n '2,12p;60,64p;/graph:/p;/single/,$p'
+  for a in "12288 12288 3 0 15 8" "11008 4096 4 128 1 8"; do OWQ_LIB=paper_2306_02272_b200/_ab/$L.so timeout 120 python tools/prof_batch.py $a 24 | grep f16; done
+done) 2>&1 | tee gpurun_out/sb9.txt
