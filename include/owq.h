@@ -212,7 +212,9 @@ owq_status owq_gemv(const owq_shape *shape, const void *d_packed,
  * d_y [B][c_out] (fp32 if y_f32).  Same arithmetic as owq_gemv; the MMA's N
  * dimension carries the 6 digit rows of every activation row (N = 8 / 16 / 32
  * / 64 / 96 for B = 1 / 2 / <= 5 / <= 10 / <= 16).  UNSUPPORTED if B is outside
- * [1, 16]. */
+ * [1, 16].  Layout-3 blobs with grouped scales at B >= 4 (c_in % 8 == 0, d_x
+ * 16-byte aligned) run owq_gemm_batch_f16's kernel instead (faster there,
+ * DESIGN.md §6.5); the result stays within the same error bound. */
 owq_status owq_gemm_small_batch(const owq_shape *shape, const void *d_packed,
                                 const uint16_t *d_x, int batch, void *d_y,
                                 int y_f32, void *d_workspace, size_t ws_bytes,

@@ -1589,6 +1589,14 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
     return cc::gemm(cc::make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak, Ks), d_packed, d_x, B, d_y,
                     y_f32, d_ws, ws_bytes, grid_req, (cudaStream_t)stream);
   const Geo g = make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak);
+  // Grouped scales at B >= 4: the fp16-A batch kernel is faster (DESIGN.md §6.5:
+  // LLaMA-7B up g128 B = 8 27.5 vs 57 us); an explicit grid request keeps this kernel.
+  if (grid_req == 0 && g.group && B >= 4 && !(s->c_in & 7) && !(reinterpret_cast<uintptr_t>(d_x) & 15) &&
+      ws_bytes >= ws_sync()) {
+    const owq_status r = pf::sb::launch(g, d_packed, d_x, B, d_y, y_f32, (uint8_t*)d_ws + ws_sync(),
+                                        ws_bytes - ws_sync(), device_sms(), (cudaStream_t)stream);
+    if (r == OWQ_OK || r == OWQ_ERR_CUDA) return r;   // else (unsupported group / workspace): this kernel
+  }
   const int64_t grid = grid_for(g, grid_req);
   if (grid > kMaxGrid || (int64_t)g.nrb * items_per_rb(g) >= (1ll << 31)) return OWQ_ERR_UNSUPPORTED;
   if (ws_bytes < ws_bytes_for(g, B, grid)) return OWQ_ERR_BUFFER_TOO_SMALL;

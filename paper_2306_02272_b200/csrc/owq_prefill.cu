@@ -96,6 +96,20 @@ __device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
   return d;
 }
 
+#ifdef OWQ_EXPERIMENTS
+// per-stage clock64 stamps of CTA (0, 0): events 0 producer after empty, 1 decode
+// after full, 2 decode arrive, 3 MMA after afull, 4 MMA after bfull, 5 loader after
+// empty, 6 loader arrive; per CTA: globaltimer start, loader pdl done, dfull seen, exit
+__device__ long long g_pf_trace[8][256];
+__device__ unsigned long long g_pf_cta[4][2048];
+#define PF_TR(ev, l) do { if (blockIdx.x == 0 && blockIdx.y == 0 && (l) < 256) g_pf_trace[ev][l] = clock64(); } while (0)
+#define PF_CTA(ev) do { const int c_ = blockIdx.y * gridDim.x + blockIdx.x; unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); if (c_ < 2048) g_pf_cta[ev][c_] = t_; } while (0)
+#else
+#define PF_TR(ev, l) do { } while (0)
+#define PF_CTA(ev) do { } while (0)
+#endif
+
 template <int BITS>
 __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -134,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
   tc_fence_after();
   const uint32_t tmem = *tslot;
   const uint32_t ssb = (uint32_t)g.ss_bytes;
+  if (threadIdx.x == 0) PF_CTA(0);
 
   if (warp == kProdW) {
     // ------------------------------------------------ producer: codes of each super-step (TMA bulk)
@@ -142,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
       for (int ss = 0; ss < nss; ++ss) {
         const int s = ss % NST;
         if (ss >= NST) mbar_wait(&empty[s], (uint32_t)((ss / NST) - 1) & 1u);
+        PF_TR(0, ss);
         mbar_expect_tx(&full[s], ssb * nrb_here);
         for (int h = 0; h < nrb_here; ++h)
           bulk_g2s(Cd(s, h), p.blob + g.units_off + item_offset(g, rb0 + h, ss), ssb, &full[s]);
@@ -155,7 +171,9 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
       const int s = ss % NST;
       const uint32_t ph = (uint32_t)(ss / NST) & 1u;
       mbar_wait(&afull[s], ph);
+      if (lane == 0) PF_TR(3, ss);
       mbar_wait(&bfull[s], ph);
+      if (lane == 0) PF_TR(4, ss);
       fence_proxy_async();   // the landed cp.async (generic-proxy) writes, before the MMA's async-proxy reads
       tc_fence_after();
       if (lane == 0) {
@@ -186,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
     for (int ss = 0; ss < nss; ++ss) {
       const int s = ss % NST;
       mbar_wait(&full[s], (uint32_t)(ss / NST) & 1u);
+      if (threadIdx.x == 0) PF_TR(1, ss);
       if (!live) {          // the CTA's second row-block does not exist: nothing to decode
         mbar_arrive(&afull[s]);
         continue;
@@ -209,38 +228,80 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
       }
       fence_proxy_async();
       mbar_arrive(&afull[s]);
+      if (threadIdx.x == 0) PF_TR(2, ss);
     }
-    // ---- epilogue (the decode warps): thread = row, TMEM lane quarter = warp % 4, D_h
-    if (!live) goto done;
+    // ---- epilogue (the decode warps): thread = row, TMEM lane quarter = warp % 4, D_h.
+    // The weak fold reads x at the weak columns from shared memory: per 16 tokens
+    // the 8 warps gather x[tokens][widx] once (k x 16 values), and the rows' fp16
+    // weak values are staged once when they fit.  (Round 2's first version loaded
+    // both from global memory inside the token loop: 200+ us of a 500 us CTA at
+    // 12288^2 x 2048 tokens, tools/pf_trace.py.)  The ring is free once dfull
+    // completed (all MMAs done), so the staging reuses it.
     {
     const int q = warp & 3;
+    const int et = threadIdx.x;                      // 0 .. 8 x 32 - 1 (decode warps)
+    constexpr int kEpiT = kDecW * 32;
     const int64_t tok0 = (int64_t)tile * NT;
     const int64_t grow = (int64_t)rb * kRowBlock + r;
-    const uint32_t szw = __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off + (int64_t)rb * kSZBlockBytes) + r);
+    const uint32_t szw = live ? __ldg(reinterpret_cast<const uint32_t*>(p.blob + g.sz_off + (int64_t)rb * kSZBlockBytes) + r) : 0u;
     const float sc = __low2float(*reinterpret_cast<const __half2*>(&szw));
     pdl_wait();   // y (and x) belong to earlier kernels until they complete
     mbar_wait(dfull, 0);
+    if (threadIdx.x == 0) PF_CTA(2);
     tc_fence_after();
     const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
     const uint8_t* wrec = p.blob + g.units_off + (int64_t)rb * g.rb_bytes + (int64_t)g.nss * g.ss_bytes;
+    const int k = g.k;
+    auto wval = [&](int tt) {
+      const int ch = tt / kWeakChunk, c = tt % kWeakChunk;
+      return ch < g.nfull ? *reinterpret_cast<const __half*>(wrec + (int64_t)ch * kWeakChunkBytes + (r * kWeakChunk + c) * 2)
+                          : *reinterpret_cast<const __half*>(wrec + (int64_t)g.nfull * kWeakChunkBytes + (r * g.ktail + c) * 2);
+    };
+    // x at the weak columns: all NT tokens at once when they fit next to the staged
+    // weak values ([c16][k][16]), else one token group at a time ([k][16])
+    const size_t ring = (size_t)NST * STAGE;
+    const bool xall = (size_t)k * NT * 2 + 128 + (size_t)RB * k * 256 <= ring;
+    const size_t xw_bytes = ((size_t)k * (xall ? NT : 16) * 2 + 127) & ~(size_t)127;
+    __half* xw = reinterpret_cast<__half*>(base);
+    __half* wsm = reinterpret_cast<__half*>(base + xw_bytes);        // [RB][k][128]
+    const bool wstaged = xw_bytes + (size_t)RB * k * 256 <= ring;
+    if (wstaged && live)
+      for (int tt = 0; tt < k; ++tt) wsm[((size_t)h * k + tt) * 128 + r] = wval(tt);
+    auto gather = [&](int c0, int nc) {   // token groups c0 .. c0 + nc - 1 -> xw[(c - c0)][tt][16]
+      for (int i = et; i < nc * k * 16; i += kEpiT) {
+        const int c = i / (k * 16), rem = i - c * k * 16, tt = rem >> 4, jj = rem & 15;
+        const int64_t n = tok0 + (c0 + c) * 16 + jj;
+        xw[i] = n < p.B ? p.x[n * g.K + __ldg(widx + tt)] : __float2half(0.f);
+      }
+    };
+    if (xall) {
+      gather(0, NT / 16);
+      named_sync(1, kEpiT);
+    }
     for (int c16 = 0; c16 < NT / 16; ++c16) {
+      if (!xall) {
+        named_sync(1, kEpiT);   // the previous token group's readers are done with xw (and wsm is written)
+        gather(c16, 1);
+        named_sync(1, kEpiT);
+      }
+      if (!live) continue;
+      const __half* xg = xw + (xall ? (size_t)c16 * k * 16 : 0);
       uint32_t d[16];
       tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16), d);
       float v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) v[j] = sc * __uint_as_float(d[j]);
       // fp16 weak columns x the tokens' fp16 activations at their indices
-      for (int tt = 0; tt < g.k; ++tt) {
-        const int ch = tt / kWeakChunk, c = tt % kWeakChunk;
-        const __half wv = ch < g.nfull
-                              ? *reinterpret_cast<const __half*>(wrec + (int64_t)ch * kWeakChunkBytes + (r * kWeakChunk + c) * 2)
-                              : *reinterpret_cast<const __half*>(wrec + (int64_t)g.nfull * kWeakChunkBytes + (r * g.ktail + c) * 2);
-        const float wf = __half2float(wv);
-        const int j = __ldg(widx + tt);
+      for (int tt = 0; tt < k; ++tt) {
+        const float wf = __half2float(wstaged ? wsm[((size_t)h * k + tt) * 128 + r] : wval(tt));
+        const uint4* xv = reinterpret_cast<const uint4*>(xg + tt * 16);
+        const uint4 x0 = xv[0], x1 = xv[1];
+        const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int64_t n = tok0 + c16 * 16 + jj;
-          if (n < p.B) v[jj] = fmaf(wf, __half2float(p.x[n * g.K + j]), v[jj]);
+        for (int c = 0; c < 8; ++c) {
+          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&xs[c]));
+          v[2 * c] = fmaf(wf, f.x, v[2 * c]);
+          v[2 * c + 1] = fmaf(wf, f.y, v[2 * c + 1]);
         }
       }
       if (grow < g.M)
@@ -262,9 +323,11 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
     constexpr int LT = kLoadW * 32;
     const int64_t tok0 = (int64_t)tile * NT;
     pdl_wait();   // x belongs to earlier kernels until they complete
+    if (t == 0) PF_CTA(1);
     for (int ss = 0; ss < nss; ++ss) {
       const int s = ss % NST;
       if (ss >= NST) mbar_wait(&empty[s], (uint32_t)((ss / NST) - 1) & 1u);
+      if (t == 0) PF_TR(5, ss);
       const uint32_t b0 = smem_u32(Bt(s));
 #pragma unroll 4
       for (int e = t; e < NT * 8; e += LT) {   // 16-byte chunks: token n, K-chunk kc
@@ -275,16 +338,17 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
         cp_async16(b0 + (uint32_t)kc * (NT * 16) + (uint32_t)(n >> 3) * 128u + (uint32_t)(n & 7) * 16u, src, ok ? 16u : 0u);
       }
       cp_async_arrive_noinc(&bfull[s]);
+      if (t == 0) PF_TR(6, ss);
     }
     cp_async_wait_all();
   }
-done:
   tc_fence_before();
   __syncthreads();
   if (warp == kProdW) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
+  if (threadIdx.x == 0) PF_CTA(3);
 }
 
 owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, cudaStream_t stream) {
@@ -666,23 +730,37 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
   if (threadIdx.x == 0) SB_CTA(2);
 }
 
-// splits of K (in super-steps, on group boundaries): as many as fit one wave of
-// `slots` resident CTAs (round 2 rounded up to 2 x SMs, which left a short
-// second wave -- e.g. 344 CTAs for LLaMA-7B up -- at 1 CTA per SM)
+// Splits of K (in super-steps, on drain-group boundaries): the split length that
+// minimises the makespan  waves x (split / K + c)  over `slots` resident CTAs,
+// c = 0.05 being a CTA's fixed cost (prologue, pipeline fill, fixup) relative to
+// a full-K CTA.  (One CTA per row-block left 52 of 148 SMs idle at 12288^2;
+// round 2's first planner rounded up to 2 x SMs and left a short second wave.)
 static void plan(const Geo& g, int slots, int& KS, int& sps, int& gss) {
   gss = g.group ? g.group / 64 : kDrainSS;
   const int unit = gss;
   const int units = (g.nss + unit - 1) / unit;
-  int want = std::max(1, slots / g.nrb);
-  want = std::min(want, units);
-  const int upc = (units + want - 1) / want;   // units per split
-  sps = upc * unit;
+  double best = 1e30;
+  KS = 1;
+  sps = units * unit;
+  for (int upc = units; upc >= 1; --upc) {
+    const int ks = (units + upc - 1) / upc;
+    if (ks > 64) break;
+    const int64_t waves = ((int64_t)ks * g.nrb + slots - 1) / slots;
+    const double cost = (double)waves * ((double)upc / units + 0.05);
+    if (cost < best - 1e-9) {
+      best = cost;
+      KS = ks;
+      sps = upc * unit;
+    }
+  }
   KS = (g.nss + sps - 1) / sps;
 }
 
 size_t workspace_bytes(const Geo& g, int B, int sms) {
-  int KS, sps, gss;
-  plan(g, 2 * sms, KS, sps, gss);   // at most two resident CTAs per SM (launch_t)
+  int KS, KS2, sps, gss;
+  plan(g, sms, KS, sps, gss);       // one or two resident CTAs per SM (launch_t)
+  plan(g, 2 * sms, KS2, sps, gss);
+  KS = std::max(KS, KS2);
   return (size_t)g.nrb * 4 + 256 + (KS > 1 ? (size_t)KS * B * g.nrb * kRowBlock * 4 : 0);
 }
 
@@ -717,7 +795,11 @@ static owq_status launch_t(Params& p, int sms, cudaStream_t stream) {
     }
 #endif
   }
-  plan(p.g, occupancy[dev & 15] * sms, p.KS, p.sps, p.gss);
+  int slots = occupancy[dev & 15] * sms;
+#ifdef OWQ_EXPERIMENTS
+  if (const char* v = getenv("OWQ_SB_SLOTS")) slots = atoi(v);
+#endif
+  plan(p.g, slots, p.KS, p.sps, p.gss);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -765,6 +847,12 @@ owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void
 #ifdef OWQ_EXPERIMENTS
 extern "C" int owq_exp_sb_trace(long long* host) {
   return (int)cudaMemcpyFromSymbol(host, owq::pf::sb::g_sb_trace, sizeof(owq::pf::sb::g_sb_trace));
+}
+extern "C" int owq_exp_pf_trace(long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, owq::pf::g_pf_trace, sizeof(owq::pf::g_pf_trace));
+}
+extern "C" int owq_exp_pf_cta(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, owq::pf::g_pf_cta, sizeof(owq::pf::g_pf_cta));
 }
 extern "C" int owq_exp_sb_cta(unsigned long long* host) {
   return (int)cudaMemcpyFromSymbol(host, owq::pf::sb::g_sb_cta, sizeof(owq::pf::sb::g_sb_cta));
