@@ -35,6 +35,9 @@
 #include <algorithm>
 #include <cstdio>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "owq.h"
 #include "owq_layout.h"
 #include "owq_ptx.cuh"
@@ -52,12 +55,13 @@ constexpr uint32_t B_BYTES = NT * 64 * 2;        // 32 KB: [8 K-chunks][NT/8 gro
 constexpr uint32_t C_MAX = 128 * 8 * 4;          // codes of one row-block super-step (4-bit: 8 words per row)
 constexpr uint32_t STAGE = RB * A_BYTES + B_BYTES + RB * C_MAX;
 constexpr int kDecW = 4 * RB;            // decode (then epilogue) warps: thread = row
-constexpr int kLoadW = 4;                // x loader warps
+constexpr int kLoadW = 1;                // x loader warp (one lane issues the TMA tile loads)
 constexpr int kProdW = kDecW + kLoadW, kMmaW = kProdW + 1;
 constexpr int kThreads = (kMmaW + 1) * 32;
 constexpr uint32_t kSmem = NST * STAGE + 1024 + 256;
 
 struct Params {
+  CUtensorMap xmap;    // x [B][K] fp16, box 64 columns x NT tokens, 128-byte swizzle (zero fill out of range)
   const uint8_t* blob;
   const __half* x;     // [B][K]
   void* y;             // [B][M]
@@ -111,7 +115,7 @@ __device__ unsigned long long g_pf_cta[4][2048];
 #endif
 
 template <int BITS>
-__global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geo& g = p.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -121,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + NST * STAGE);
   uint64_t* full = bars;               // codes landed (TMA tx)
   uint64_t* afull = full + NST;        // A tiles written (RB x 128 threads)
-  uint64_t* bfull = afull + NST;       // B tile written (loader lanes)
+  uint64_t* bfull = afull + NST;       // B tile landed (TMA tx)
   uint64_t* empty = bfull + NST;       // the stage's MMAs completed (tcgen05.commit)
   uint64_t* dfull = empty + NST;       // all MMAs completed
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dfull + 1);
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
     for (int s = 0; s < NST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&afull[s], RB * 128);
-      mbar_init(&bfull[s], kLoadW * 32);
+      mbar_init(&bfull[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(dfull, 1);
@@ -174,16 +178,15 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
       if (lane == 0) PF_TR(3, ss);
       mbar_wait(&bfull[s], ph);
       if (lane == 0) PF_TR(4, ss);
-      fence_proxy_async();   // the landed cp.async (generic-proxy) writes, before the MMA's async-proxy reads
       tc_fence_after();
       if (lane == 0) {
         const uint32_t b0 = smem_u32(Bt(s));
         for (int h = 0; h < nrb_here; ++h) {
           const uint32_t a0 = smem_u32(A(s, h));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)   // K = 16 per MMA = two 8-element core-matrix columns
+          for (int kk = 0; kk < 4; ++kk)   // K = 16 per MMA: A two 8-element core-matrix columns, B 32 bytes into each swizzled row
             tc_mma_f16_ss(tmem + (uint32_t)(h * NT), umma_desc(a0 + kk * 2 * 2048, 2048, 128),
-                          umma_desc(b0 + kk * 2 * (NT * 16), NT * 16, 128), idesc, (ss | kk) != 0 ? 1u : 0u);
+                          umma_desc_sw128(b0 + kk * 32), idesc, (ss | kk) != 0 ? 1u : 0u);
         }
         tc_commit(&empty[s]);
         if (ss == nss - 1) tc_commit(dfull);
@@ -258,55 +261,86 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
                           : *reinterpret_cast<const __half*>(wrec + (int64_t)g.nfull * kWeakChunkBytes + (r * g.ktail + c) * 2);
     };
     // x at the weak columns: all NT tokens at once when they fit next to the staged
-    // weak values ([c16][k][16]), else one token group at a time ([k][16])
+    // weak values ([c16][k][16]), else one token group at a time ([k][16]); the
+    // weak indices are staged too.  Loads are issued four at a time (the loops
+    // were latency-bound on one dependent global load per element).
     const size_t ring = (size_t)NST * STAGE;
-    const bool xall = (size_t)k * NT * 2 + 128 + (size_t)RB * k * 256 <= ring;
+    const size_t wis_bytes = ((size_t)k * 2 + 127) & ~(size_t)127;
+    const bool xall = (size_t)k * NT * 2 + 128 + (size_t)RB * k * 256 + wis_bytes <= ring;
     const size_t xw_bytes = ((size_t)k * (xall ? NT : 16) * 2 + 127) & ~(size_t)127;
-    __half* xw = reinterpret_cast<__half*>(base);
-    __half* wsm = reinterpret_cast<__half*>(base + xw_bytes);        // [RB][k][128]
-    const bool wstaged = xw_bytes + (size_t)RB * k * 256 <= ring;
+    uint16_t* wis = reinterpret_cast<uint16_t*>(base);                      // [k] weak indices
+    __half* xw = reinterpret_cast<__half*>(base + wis_bytes);
+    __half* wsm = reinterpret_cast<__half*>(base + wis_bytes + xw_bytes);  // [RB][k][128]
+    const bool wstaged = wis_bytes + xw_bytes + (size_t)RB * k * 256 <= ring;
+    for (int tt = et; tt < k; tt += kEpiT) wis[tt] = __ldg(widx + tt);
     if (wstaged && live)
-      for (int tt = 0; tt < k; ++tt) wsm[((size_t)h * k + tt) * 128 + r] = wval(tt);
+      for (int t0 = 0; t0 < k; t0 += 4) {
+        __half wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) wv[u] = t0 + u < k ? wval(t0 + u) : __float2half(0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (t0 + u < k) wsm[((size_t)h * k + t0 + u) * 128 + r] = wv[u];
+      }
+    named_sync(1, kEpiT);   // wis (and wsm) written
     auto gather = [&](int c0, int nc) {   // token groups c0 .. c0 + nc - 1 -> xw[(c - c0)][tt][16]
-      for (int i = et; i < nc * k * 16; i += kEpiT) {
-        const int c = i / (k * 16), rem = i - c * k * 16, tt = rem >> 4, jj = rem & 15;
-        const int64_t n = tok0 + (c0 + c) * 16 + jj;
-        xw[i] = n < p.B ? p.x[n * g.K + __ldg(widx + tt)] : __float2half(0.f);
+      const int total = nc * k * 16;
+      for (int i0 = et; i0 < total; i0 += 4 * kEpiT) {
+        __half xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kEpiT;
+          xv[u] = __float2half(0.f);
+          if (i < total) {
+            const int c = i / (k * 16), rem = i - c * k * 16, tt = rem >> 4, jj = rem & 15;
+            const int64_t n = tok0 + (c0 + c) * 16 + jj;
+            if (n < p.B) xv[u] = p.x[n * g.K + wis[tt]];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u * kEpiT < total) xw[i0 + u * kEpiT] = xv[u];
       }
     };
     if (xall) {
       gather(0, NT / 16);
       named_sync(1, kEpiT);
     }
-    for (int c16 = 0; c16 < NT / 16; ++c16) {
+    // two token groups per pass: two TMEM loads behind one wait, each weak value read once
+    for (int c16 = 0; c16 < NT / 16; c16 += 2) {
       if (!xall) {
-        named_sync(1, kEpiT);   // the previous token group's readers are done with xw (and wsm is written)
-        gather(c16, 1);
+        named_sync(1, kEpiT);   // the previous token groups' readers are done with xw
+        gather(c16, 2);
         named_sync(1, kEpiT);
       }
       if (!live) continue;
       const __half* xg = xw + (xall ? (size_t)c16 * k * 16 : 0);
-      uint32_t d[16];
-      tc_ld16(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16), d);
-      float v[16];
+      uint32_t d[32];
+      tc_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16), d);
+      tc_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16 + 16), d + 16);
+      tc_wait_ld32(d);
+      float v[32];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = sc * __uint_as_float(d[j]);
+      for (int j = 0; j < 32; ++j) v[j] = sc * __uint_as_float(d[j]);
       // fp16 weak columns x the tokens' fp16 activations at their indices
       for (int tt = 0; tt < k; ++tt) {
         const float wf = __half2float(wstaged ? wsm[((size_t)h * k + tt) * 128 + r] : wval(tt));
-        const uint4* xv = reinterpret_cast<const uint4*>(xg + tt * 16);
-        const uint4 x0 = xv[0], x1 = xv[1];
-        const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&xs[c]));
-          v[2 * c] = fmaf(wf, f.x, v[2 * c]);
-          v[2 * c + 1] = fmaf(wf, f.y, v[2 * c + 1]);
+        for (int gq = 0; gq < 2; ++gq) {
+          const uint4* xv = reinterpret_cast<const uint4*>(xg + ((size_t)gq * k + tt) * 16);
+          const uint4 x0 = xv[0], x1 = xv[1];
+          const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&xs[c]));
+            v[16 * gq + 2 * c] = fmaf(wf, f.x, v[16 * gq + 2 * c]);
+            v[16 * gq + 2 * c + 1] = fmaf(wf, f.y, v[16 * gq + 2 * c + 1]);
+          }
         }
       }
       if (grow < g.M)
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
+        for (int jj = 0; jj < 32; ++jj) {
           const int64_t n = tok0 + c16 * 16 + jj;
           if (n < p.B) {
             if (p.y_f32) reinterpret_cast<float*>(p.y)[n * g.M + grow] = v[jj];
@@ -316,31 +350,23 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const Params p
     }
     }
   } else if (warp < kProdW) {
-    // ------------------------------------------------ x loaders: cp.async, up to NST stages in flight;
-    // each lane's copies of a stage arrive on bfull when they land (round 2 published
-    // stage ss - 1 after a cp.async.wait_group at stage ss: one stage of lookahead)
-    const int t = threadIdx.x - kDecW * 32;
-    constexpr int LT = kLoadW * 32;
+    // ------------------------------------------------ x loader: one lane, TMA tensor tiles of
+    // 64 columns x NT tokens in the 128-byte-swizzled K-major layout the MMA reads
+    // (round 2's first version used 4 warps of 16-byte cp.async, whose issue
+    // stalled behind the decode warps' shared-memory stores)
     const int64_t tok0 = (int64_t)tile * NT;
-    pdl_wait();   // x belongs to earlier kernels until they complete
-    if (t == 0) PF_CTA(1);
-    for (int ss = 0; ss < nss; ++ss) {
-      const int s = ss % NST;
-      if (ss >= NST) mbar_wait(&empty[s], (uint32_t)((ss / NST) - 1) & 1u);
-      if (t == 0) PF_TR(5, ss);
-      const uint32_t b0 = smem_u32(Bt(s));
-#pragma unroll 4
-      for (int e = t; e < NT * 8; e += LT) {   // 16-byte chunks: token n, K-chunk kc
-        const int n = e >> 3, kc = e & 7;
-        const int64_t col = (int64_t)ss * 64 + kc * 8;
-        const bool ok = tok0 + n < p.B && col < g.K;
-        const __half* src = ok ? p.x + (tok0 + n) * g.K + col : p.x;
-        cp_async16(b0 + (uint32_t)kc * (NT * 16) + (uint32_t)(n >> 3) * 128u + (uint32_t)(n & 7) * 16u, src, ok ? 16u : 0u);
+    if (lane == 0) {
+      pdl_wait();   // x belongs to earlier kernels until they complete
+      PF_CTA(1);
+      for (int ss = 0; ss < nss; ++ss) {
+        const int s = ss % NST;
+        if (ss >= NST) mbar_wait(&empty[s], (uint32_t)((ss / NST) - 1) & 1u);
+        PF_TR(5, ss);
+        mbar_expect_tx(&bfull[s], B_BYTES);
+        tma_load_2d(Bt(s), &p.xmap, ss * 64, (int)tok0, &bfull[s]);
+        PF_TR(6, ss);
       }
-      cp_async_arrive_noinc(&bfull[s]);
-      if (t == 0) PF_TR(6, ss);
     }
-    cp_async_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -359,6 +385,28 @@ owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void
   p.g = g;
   p.B = B;
   p.y_f32 = y_f32 ? 1 : 0;
+  {
+    // x as a 2-D tensor map: dims {K, B}, row pitch 2K bytes (K % 8 == 0 checked by
+    // the caller), box {64, NT}, 128-byte swizzle; rows past B and columns past K
+    // read as zero.  The driver entry point is looked up once.
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess || !fn)
+        return OWQ_ERR_CUDA;
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)g.K, (cuuint64_t)B};
+    const cuuint64_t strides[1] = {(cuuint64_t)g.K * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)NT};
+    const cuuint32_t estr[2] = {1, 1};
+    if (encode(&p.xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<uint16_t*>(x), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return OWQ_ERR_CUDA;
+  }
   auto kern = g.bits == 3 ? owq_prefill_kernel<3> : owq_prefill_kernel<4>;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -778,21 +826,21 @@ static owq_status launch_t(Params& p, int sms, cudaStream_t stream) {
     // CTA (measured: 1 resident CTA per SM at 92 KB)
     if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100) != cudaSuccess)
       return OWQ_ERR_CUDA;
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1)
-      return OWQ_ERR_CUDA;
-    occupancy[dev & 15] = std::min(occ, 2);   // workspace_bytes() assumes at most 2
+    // Resident CTAs per SM from shared memory and registers: the occupancy API
+    // reports 1 for any kernel that allocates TMEM (tools/occ_probe.cu), but two
+    // 128-column allocations fit and two CTAs were measured resident at once
+    // (tools/sb_trace.py: 288 CTAs started within 0.8 us on 148 SMs).
+    cudaFuncAttributes fa{};
+    if (cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return OWQ_ERR_CUDA;
+    int smem_sm = 0, regs_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+    int occ = std::min<int>(2, smem_sm / (int)(smem + 1024));   // workspace_bytes() assumes at most 2
+    while (occ > 1 && occ * fa.numRegs * kThreads > regs_sm) --occ;
+    occupancy[dev & 15] = std::max(occ, 1);
 #ifdef OWQ_EXPERIMENTS
-    {
-      int o0 = 0, o1 = 0, o2 = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, kern, kThreads, 0);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, kern, kThreads, 48 * 1024);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, kern, 32, smem);
-      cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, kern);
-      fprintf(stderr, "owq sb<%d,%d>: %d resident CTAs per SM (smem %u, threads %d); smem 0: %d, 48K: %d, 32 thr: %d; regs %d static %zu maxdyn %d\n",
-              BITS, NT, occ, smem, kThreads, o0, o1, o2, fa.numRegs, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes);
-    }
+    fprintf(stderr, "owq sb<%d,%d>: %d resident CTAs per SM (smem %u, threads %d, regs %d)\n", BITS, NT, occupancy[dev & 15],
+            smem, kThreads, fa.numRegs);
 #endif
   }
   int slots = occupancy[dev & 15] * sms;

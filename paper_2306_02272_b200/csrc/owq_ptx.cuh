@@ -95,12 +95,44 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t* d) {
       : "memory");
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tc_ld16_nowait(uint32_t taddr, uint32_t* d) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+        "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+      : "r"(taddr)
+      : "memory");
+}
+// wait for earlier tcgen05.ld; the 32 destination registers are tied to the wait so
+// no use of them can be scheduled before it
+__device__ __forceinline__ void tc_wait_ld32(uint32_t* d) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3]), "+r"(d[4]), "+r"(d[5]), "+r"(d[6]), "+r"(d[7]), "+r"(d[8]), "+r"(d[9]), "+r"(d[10]), "+r"(d[11]), "+r"(d[12]), "+r"(d[13]), "+r"(d[14]), "+r"(d[15]), "+r"(d[16]), "+r"(d[17]), "+r"(d[18]), "+r"(d[19]), "+r"(d[20]), "+r"(d[21]), "+r"(d[22]), "+r"(d[23]), "+r"(d[24]), "+r"(d[25]), "+r"(d[26]), "+r"(d[27]), "+r"(d[28]), "+r"(d[29]), "+r"(d[30]), "+r"(d[31])
+               :
+               : "memory");
+}
 // UMMA shared-memory descriptor, K-major, no swizzle (sm_100 descriptor version 1):
 // start address, LBO = byte distance between core matrices adjacent in K,
 // SBO = byte distance between core matrices adjacent in M / N (8-row groups)
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: rows of 128 bytes
+// (64 fp16 along K) in 8-row atoms of 1024 bytes (SBO); LBO unused (1); layout
+// type 2 (SWIZZLE_128B) in bits 61-63; a K step inside the row advances the start
+// address (the hardware applies the XOR on the computed addresses)
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+// 2-D TMA tensor tile load (coordinates: innermost first) completing on `bar`
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
 // instruction descriptor, kind::f16: D f32, A f16, B f16, both K-major, M x N
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
