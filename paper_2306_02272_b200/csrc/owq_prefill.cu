@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_c
     pdl_wait();   // y (and x) belong to earlier kernels until they complete
     mbar_wait(dfull, 0);
     if (threadIdx.x == 0) PF_CTA(2);
+    if (threadIdx.x == 0) PF_TR(7, 15);
     tc_fence_after();
     const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
     const uint8_t* wrec = p.blob + g.units_off + (int64_t)rb * g.rb_bytes + (int64_t)g.nss * g.ss_bytes;
@@ -262,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_c
     };
     // x at the weak columns: all NT tokens at once when they fit next to the staged
     // weak values ([c16][k][16]), else one token group at a time ([k][16]); the
-    // weak indices are staged too.  Loads are issued four at a time (the loops
+    // weak indices are staged too.  Loads are issued four / eight at a time (the loops
     // were latency-bound on one dependent global load per element).
     const size_t ring = (size_t)NST * STAGE;
     const size_t wis_bytes = ((size_t)k * 2 + 127) & ~(size_t)127;
@@ -283,12 +284,13 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_c
           if (t0 + u < k) wsm[((size_t)h * k + t0 + u) * 128 + r] = wv[u];
       }
     named_sync(1, kEpiT);   // wis (and wsm) written
+    if (et == 0) PF_TR(7, 0);
     auto gather = [&](int c0, int nc) {   // token groups c0 .. c0 + nc - 1 -> xw[(c - c0)][tt][16]
       const int total = nc * k * 16;
-      for (int i0 = et; i0 < total; i0 += 4 * kEpiT) {
-        __half xv[4];
+      for (int i0 = et; i0 < total; i0 += 8 * kEpiT) {
+        __half xv[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < 8; ++u) {
           const int i = i0 + u * kEpiT;
           xv[u] = __float2half(0.f);
           if (i < total) {
@@ -298,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_c
           }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 8; ++u)
           if (i0 + u * kEpiT < total) xw[i0 + u * kEpiT] = xv[u];
       }
     };
@@ -306,47 +308,96 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_c
       gather(0, NT / 16);
       named_sync(1, kEpiT);
     }
-    // two token groups per pass: two TMEM loads behind one wait, each weak value read once
+    if (et == 0) PF_TR(7, 1);
+    // two token groups per pass: two TMEM loads behind one wait, each weak value read
+    // once, the fold as FFMA2 pairs; the pass's 32 tokens x 256 rows of y are staged
+    // in shared memory and written as 16-byte vectors along the rows (each warp
+    // writing 2-byte elements of 32 rows per token measured ~4000 cycles per pass).
+    const int ysz = p.y_f32 ? 4 : 2;
+    uint8_t* ystage = base + wis_bytes + xw_bytes + (wstaged ? (((size_t)RB * k * 256 + 127) & ~(size_t)127) : 0);
+    const bool ystaged = (size_t)(ystage - base) + (size_t)32 * RB * 128 * ysz <= ring;
+    const int rows_here = nrb_here * 128;
     for (int c16 = 0; c16 < NT / 16; c16 += 2) {
       if (!xall) {
         named_sync(1, kEpiT);   // the previous token groups' readers are done with xw
         gather(c16, 2);
         named_sync(1, kEpiT);
+      } else if (ystaged) {
+        named_sync(1, kEpiT);   // the previous pass's ystage readers are done
       }
-      if (!live) continue;
-      const __half* xg = xw + (xall ? (size_t)c16 * k * 16 : 0);
-      uint32_t d[32];
-      tc_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16), d);
-      tc_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16 + 16), d + 16);
-      tc_wait_ld32(d);
-      float v[32];
+      if (live) {
+        const __half* xg = xw + (xall ? (size_t)c16 * k * 16 : 0);
+        uint32_t d[32];
+        tc_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16), d);
+        tc_ld16_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NT + c16 * 16 + 16), d + 16);
+        tc_wait_ld32(d);
+        float v[32];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = sc * __uint_as_float(d[j]);
-      // fp16 weak columns x the tokens' fp16 activations at their indices
-      for (int tt = 0; tt < k; ++tt) {
-        const float wf = __half2float(wstaged ? wsm[((size_t)h * k + tt) * 128 + r] : wval(tt));
+        for (int j = 0; j < 32; ++j) v[j] = sc * __uint_as_float(d[j]);
+        // fp16 weak columns x the tokens' fp16 activations at their indices
+        for (int tt = 0; tt < k; ++tt) {
+          const float wf = __half2float(wstaged ? wsm[((size_t)h * k + tt) * 128 + r] : wval(tt));
+          const unsigned long long wf2 = ((unsigned long long)__float_as_uint(wf) << 32) | __float_as_uint(wf);
 #pragma unroll
-        for (int gq = 0; gq < 2; ++gq) {
-          const uint4* xv = reinterpret_cast<const uint4*>(xg + ((size_t)gq * k + tt) * 16);
-          const uint4 x0 = xv[0], x1 = xv[1];
-          const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          for (int gq = 0; gq < 2; ++gq) {
+            const uint4* xv = reinterpret_cast<const uint4*>(xg + ((size_t)gq * k + tt) * 16);
+            const uint4 x0 = xv[0], x1 = xv[1];
+            const uint32_t xs[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&xs[c]));
-            v[16 * gq + 2 * c] = fmaf(wf, f.x, v[16 * gq + 2 * c]);
-            v[16 * gq + 2 * c + 1] = fmaf(wf, f.y, v[16 * gq + 2 * c + 1]);
+            for (int c = 0; c < 8; ++c) {
+              const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&xs[c]));
+              const unsigned long long fx = ((unsigned long long)__float_as_uint(f.y) << 32) | __float_as_uint(f.x);
+              float& a0 = v[16 * gq + 2 * c];
+              float& a1 = v[16 * gq + 2 * c + 1];
+              unsigned long long acc = ((unsigned long long)__float_as_uint(a1) << 32) | __float_as_uint(a0);
+              asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(wf2), "l"(fx));
+              a0 = __uint_as_float((uint32_t)acc);
+              a1 = __uint_as_float((uint32_t)(acc >> 32));
+            }
+          }
+        }
+        if (ystaged) {
+          // ystage[token j][row h*128 + r]
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const size_t o = ((size_t)jj * RB * 128 + (size_t)h * 128 + r) * ysz;
+            if (p.y_f32) *reinterpret_cast<float*>(ystage + o) = v[jj];
+            else *reinterpret_cast<__half*>(ystage + o) = __float2half_rn(v[jj]);
+          }
+        } else if (grow < g.M) {
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int64_t n = tok0 + c16 * 16 + jj;
+            if (n < p.B) {
+              if (p.y_f32) reinterpret_cast<float*>(p.y)[n * g.M + grow] = v[jj];
+              else reinterpret_cast<__half*>(p.y)[n * g.M + grow] = __float2half_rn(v[jj]);
+            }
           }
         }
       }
-      if (grow < g.M)
-#pragma unroll
-        for (int jj = 0; jj < 32; ++jj) {
+      if (ystaged) {
+        named_sync(1, kEpiT);   // the pass's 32 tokens are staged
+        // each token's rows_here rows are contiguous in y: 16-byte vectors, rows past M
+        // (the last row-block) element by element
+        const int vec = 16 / ysz;                       // elements per vector
+        const int per_tok = rows_here / vec;
+        for (int i = et; i < 32 * per_tok; i += kEpiT) {
+          const int jj = i / per_tok, e0 = (i - jj * per_tok) * vec;
           const int64_t n = tok0 + c16 * 16 + jj;
-          if (n < p.B) {
-            if (p.y_f32) reinterpret_cast<float*>(p.y)[n * g.M + grow] = v[jj];
-            else reinterpret_cast<__half*>(p.y)[n * g.M + grow] = __float2half_rn(v[jj]);
+          if (n >= p.B) continue;
+          const int64_t row0 = (int64_t)rb0 * 128 + e0;
+          const uint8_t* src = ystage + ((size_t)jj * RB * 128 + e0) * ysz;
+          uint8_t* dst = reinterpret_cast<uint8_t*>(p.y) + (n * g.M + row0) * ysz;
+          if (row0 + vec <= g.M && !(reinterpret_cast<uintptr_t>(dst) & 15)) {
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+          } else {
+            for (int e = 0; e < vec && row0 + e < g.M; ++e) {
+              if (p.y_f32) reinterpret_cast<float*>(dst)[e] = reinterpret_cast<const float*>(src)[e];
+              else reinterpret_cast<__half*>(dst)[e] = reinterpret_cast<const __half*>(src)[e];
+            }
           }
         }
+      }
     }
     }
   } else if (warp < kProdW) {

@@ -33,6 +33,9 @@ def run(d, x, dev, y_f32=True):
 @pytest.mark.parametrize("M,K,bits,k,B", [
     (768, 768, 3, 8, 64), (768, 768, 3, 8, 17), (300, 1000, 4, 5, 300), (1000, 2048, 3, 0, 256),
     (4096, 4096, 3, 5, 512), (130, 640, 3, 9, 2048),
+    # many weak columns: x at the weak columns staged per token group (k = 300),
+    # weak values read from global memory (k = 600)
+    (256, 4096, 3, 300, 300), (200, 8192, 4, 600, 40),
 ])
 def test_prefill_full_parity(dev, M, K, bits, k, B):
     d = synth.representation(M, K, bits, 0, k, seed=M + K + B)

@@ -11,9 +11,8 @@ import torch  # noqa: E402
 import paper_2306_02272_b200 as owq  # noqa: E402
 import synth  # noqa: E402
 
-a = [int(v) for v in sys.argv[1:]] + [12288, 12288, 2048][len(sys.argv) - 1:]
-M, K, B = a[:3]
-k = 15
+a = [int(v) for v in sys.argv[1:]] + [12288, 12288, 2048, 15][len(sys.argv) - 1:]
+M, K, B, k = a[:4]
 d = synth.representation(M, K, 3, 0, k, seed=1)
 shape = owq.Shape(M, K, 3, 0, k)
 P = owq.owq_pack(shape, d, device="cuda")
@@ -37,6 +36,9 @@ for l in list(range(0, 12)) + list(range(180, 192)):
     if not t[:, l].any():
         continue
     print(f"{l:3d} " + " ".join(f"{(v - t0) if v else -1:9d}" for v in t[:7, l]))
+e = t[7]
+print("epilogue of CTA (0,0), cycles after dfull: staged", e[0] - e[15], " gathered", e[1] - e[15], " passes",
+      [int(e[2 + i] - e[15]) for i in range(8)])
 cc = np.zeros((4, 2048), dtype=np.uint64)
 owq.lib().owq_exp_pf_cta(cc.ctypes.data_as(ctypes.c_void_p))
 n = int((cc[0] > 0).sum())
