@@ -262,13 +262,13 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_c
                           : *reinterpret_cast<const __half*>(wrec + (int64_t)g.nfull * kWeakChunkBytes + (r * g.ktail + c) * 2);
     };
     // x at the weak columns: all NT tokens at once when they fit next to the staged
-    // weak values ([c16][k][16]), else one token group at a time ([k][16]); the
+    // weak values ([c16][k][16]), else two token groups at a time ([2][k][16]); the
     // weak indices are staged too.  Loads are issued four / eight at a time (the loops
     // were latency-bound on one dependent global load per element).
     const size_t ring = (size_t)NST * STAGE;
     const size_t wis_bytes = ((size_t)k * 2 + 127) & ~(size_t)127;
     const bool xall = (size_t)k * NT * 2 + 128 + (size_t)RB * k * 256 + wis_bytes <= ring;
-    const size_t xw_bytes = ((size_t)k * (xall ? NT : 16) * 2 + 127) & ~(size_t)127;
+    const size_t xw_bytes = ((size_t)k * (xall ? NT : 32) * 2 + 127) & ~(size_t)127;   // else two token groups per pass
     uint16_t* wis = reinterpret_cast<uint16_t*>(base);                      // [k] weak indices
     __half* xw = reinterpret_cast<__half*>(base + wis_bytes);
     __half* wsm = reinterpret_cast<__half*>(base + wis_bytes + xw_bytes);  // [RB][k][128]
@@ -522,6 +522,14 @@ __device__ __forceinline__ unsigned long long sb_gtime() {
 #define OWQ_SB_NST 4
 #endif
 constexpr int NST = OWQ_SB_NST;
+#ifndef OWQ_SB_SPIN
+#define OWQ_SB_SPIN 0
+#endif
+// ring waits: parked try_wait (0) or polling test_wait (1)
+__device__ __forceinline__ void sb_wait(uint64_t* b, uint32_t parity) {
+  if (OWQ_SB_SPIN) mbar_wait_spin(b, parity);
+  else mbar_wait(b, parity);
+}
 #ifndef OWQ_SB_SUB
 #define OWQ_SB_SUB 1
 #endif
@@ -610,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
       pdl_launch_dependents();
       for (int l = 0; l < n; ++l) {
         const int s = l % NST;
-        if (l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
+        if (l >= NST) sb_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
         SB_TR(0, l);
         const uint32_t bytes = ssb * (uint32_t)nsub(l);   // consecutive super-steps are contiguous in the blob
         if (p.skip & 8) {
@@ -634,8 +642,8 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
       if (gpos == p.gss) gpos = 0;
       const int buf = gcount % NDB;
       // one lane waits (parked waiters on a barrier cost every phase change)
-      if (lane == 0 && first && gcount >= NDB) mbar_wait(&dempty[buf], (uint32_t)((gcount / NDB) - 1) & 1u);
-      if (lane == 0) mbar_wait(&afull[s], ph);   // A decoded and the x tile landed
+      if (lane == 0 && first && gcount >= NDB) sb_wait(&dempty[buf], (uint32_t)((gcount / NDB) - 1) & 1u);
+      if (lane == 0) sb_wait(&afull[s], ph);   // A decoded and the x tile landed
       if (lane == 0) SB_TR(3, l);
       if (lane == 0) SB_TR(4, l);
       if (!(p.skip & 16)) fence_proxy_async();   // the landed cp.async (generic-proxy) writes, before the MMA's async-proxy reads
@@ -686,7 +694,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
         zzw = *reinterpret_cast<const uint32_t*>(&zz);
         zg = gi;
       }
-      if (lane == 0) mbar_wait(&full[s], (uint32_t)(l / NST) & 1u);
+      if (lane == 0) sb_wait(&full[s], (uint32_t)(l / NST) & 1u);
       __syncwarp();
       if (threadIdx.x == 0) SB_TR(1, l);
       if (u < nsub(l) && !(p.skip & 1)) {
@@ -719,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
     if (lane == 0) SB_CTA(1);
     for (int l = 0; l < n; ++l) {
       const int s = l % NST;
-      if (lane == 0 && l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
+      if (lane == 0 && l >= NST) sb_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
       __syncwarp();
       if (lane == 0) SB_TR(5, l);
 #pragma unroll
@@ -757,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p
       const uint32_t szw = sznext;
       if (grouped) sznext = ldsz(gi + 1);
       const float sc = __low2float(*reinterpret_cast<const __half2*>(&szw));
-      if (lane == 0) mbar_wait(&dfull[buf], (uint32_t)(gcount / NDB) & 1u);
+      if (lane == 0) sb_wait(&dfull[buf], (uint32_t)(gcount / NDB) & 1u);
       __syncwarp();
       if (r == 0) SB_TR(7, l);
       tc_fence_after();

@@ -29,6 +29,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Non-suspending wait: polls with test_wait (never parks the thread), for waits on
+// the critical path whose wake-up latency matters more than the issue slots.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WS_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WS_%=;\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
