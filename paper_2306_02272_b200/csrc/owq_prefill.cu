@@ -565,8 +565,14 @@ struct Params {
 template <int NT>
 __host__ __device__ constexpr uint32_t stage_bytes() { return SUB * (A_BYTES + NT * 128 + C_MAX); }
 
+// two resident CTAs per SM (register cap 93: N = 32 no longer takes 125 registers
+// and one CTA per SM, 78.9 -> see DESIGN.md §6.5)
+#ifndef OWQ_SB_MINB
+#define OWQ_SB_MINB 2
+#endif
+constexpr int kMaxOcc = 3;   // resident CTAs per SM the planner and workspace_bytes() allow
 template <int BITS, int NT>
-__global__ void __launch_bounds__(kThreads, 1) owq_gemm_sb_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, OWQ_SB_MINB) owq_gemm_sb_kernel(const Params p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr uint32_t STG = stage_bytes<NT>();
   const Geo& g = p.g;
@@ -865,8 +871,10 @@ static void plan(const Geo& g, int slots, int& KS, int& sps, int& gss) {
 
 size_t workspace_bytes(const Geo& g, int B, int sms) {
   int KS, KS2, sps, gss;
-  plan(g, sms, KS, sps, gss);       // one or two resident CTAs per SM (launch_t)
+  plan(g, sms, KS, sps, gss);       // 1 .. kMaxOcc resident CTAs per SM (launch_t)
   plan(g, 2 * sms, KS2, sps, gss);
+  KS = std::max(KS, KS2);
+  plan(g, kMaxOcc * sms, KS2, sps, gss);
   KS = std::max(KS, KS2);
   return (size_t)g.nrb * 4 + 256 + (KS > 1 ? (size_t)KS * B * g.nrb * kRowBlock * 4 : 0);
 }
@@ -894,7 +902,7 @@ static owq_status launch_t(Params& p, int sms, cudaStream_t stream) {
     int smem_sm = 0, regs_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-    int occ = std::min<int>(2, smem_sm / (int)(smem + 1024));   // workspace_bytes() assumes at most 2
+    int occ = std::min<int>(kMaxOcc, smem_sm / (int)(smem + 1024));
     while (occ > 1 && occ * fa.numRegs * kThreads > regs_sm) --occ;
     occupancy[dev & 15] = std::max(occ, 1);
 #ifdef OWQ_EXPERIMENTS
