@@ -288,6 +288,34 @@ def test_concurrent_streams_partial_grids(dev):
         assert e <= TOL
 
 
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("layout", [owq.OWQ_LAYOUT_TC, owq.OWQ_LAYOUT_CC])
+def test_concurrent_full_grids(dev, layout):
+    """Two full-grid (one CTA per SM) calls running concurrently on two streams, so
+    neither grid is wholly resident.  The stream-K fixups'
+    summer is each row-block's highest-index piece, which waits only on
+    lower-index CTAs: both calls must complete and match the oracle, repeatedly."""
+    cases = [(12288, 4096, 3, 0, 15), (8192, 6144, 3, 0, 9)]
+    streams = [torch.cuda.Stream() for _ in cases]
+    runs = []
+    for i, (M, K, bits, g, k) in enumerate(cases):
+        d = synth.representation(M, K, bits, g, k, seed=500 + i)
+        x = synth.activations(1, K, seed=600 + i, outliers=d["weak_idx"][:4])
+        L = owq.OwqLinear(d, device=dev, layout=layout)
+        rows = sorted(set([0, 127, 128, M - 1] + list(np.random.default_rng(i).choice(M, 100, replace=False))))
+        runs.append(dict(L=L, x=torch.from_numpy(x).to(dev), y=torch.empty((1, M), dtype=torch.float32, device=dev),
+                         rows=rows, ref=O.matvec_rows(rep_from_synth(d), x.astype(np.float64), rows)))
+    torch.cuda.synchronize()
+    for it in range(20):
+        for sd, r in zip(streams, runs):
+            with torch.cuda.stream(sd):
+                r["L"](r["x"], y=r["y"], y_f32=True)
+    torch.cuda.synchronize()
+    for r in runs:
+        e, _ = rel_err(r["y"].cpu().numpy().astype(np.float64)[:, r["rows"]], r["ref"])
+        assert e <= TOL
+
+
 def test_workspace_sync_words_left_zero(dev):
     """One workspace shared by calls of different shapes, batches and grids --
     co-resident (zero-word slot protocol) and larger than the SM count (counter
