@@ -48,17 +48,23 @@ namespace pf {
 using namespace owq::ptx;
 
 constexpr int NT = 256;                  // tokens per CTA (MMA N)
-constexpr int RB = 2;                    // 128-row blocks per CTA (share the x tile)
-constexpr int NST = 3;                   // pipeline stages
 constexpr uint32_t A_BYTES = 128 * 64 * 2;       // 16 KB per row-block: [8 K-chunks][16 row groups][8 rows][16 B]
-constexpr uint32_t B_BYTES = NT * 64 * 2;        // 32 KB: [8 K-chunks][NT/8 groups][8 rows][16 B]
+constexpr uint32_t B_BYTES = NT * 64 * 2;        // 32 KB: 256 token rows x 128 B (128-byte swizzle)
 constexpr uint32_t C_MAX = 128 * 8 * 4;          // codes of one row-block super-step (4-bit: 8 words per row)
-constexpr uint32_t STAGE = RB * A_BYTES + B_BYTES + RB * C_MAX;
-constexpr int kDecW = 4 * RB;            // decode (then epilogue) warps: thread = row
-constexpr int kLoadW = 1;                // x loader warp (one lane issues the TMA tile loads)
-constexpr int kProdW = kDecW + kLoadW, kMmaW = kProdW + 1;
-constexpr int kThreads = (kMmaW + 1) * 32;
-constexpr uint32_t kSmem = NST * STAGE + 1024 + 256;
+// RB 128-row blocks per CTA share each x tile: 2 by default (one D of 256 TMEM
+// columns each), 1 when two-row-block CTAs would leave SMs idle (few tokens)
+template <int RB_>
+struct PfCfg {
+  static constexpr int RB = RB_;
+  static constexpr int NST = RB == 2 ? 3 : 4;                                 // pipeline stages
+  static constexpr uint32_t STAGE = RB * A_BYTES + B_BYTES + RB * C_MAX;
+  static constexpr int kDecW = 4 * RB;            // decode (then epilogue) warps: thread = row
+  static constexpr int kLoadW = 1;                // x loader warp (one lane issues the TMA tile loads)
+  static constexpr int kProdW = kDecW + kLoadW, kMmaW = kProdW + 1;
+  static constexpr int kThreads = (kMmaW + 1) * 32;
+  static constexpr uint32_t kSmem = NST * STAGE + 1024 + 256;
+  static constexpr uint32_t kTmemCols = RB * NT;
+};
 
 struct Params {
   CUtensorMap xmap;    // x [B][K] fp16, box 64 columns x NT tokens, 128-byte swizzle (zero fill out of range)
@@ -114,8 +120,11 @@ __device__ unsigned long long g_pf_cta[4][2048];
 #define PF_CTA(ev) do { } while (0)
 #endif
 
-template <int BITS>
-__global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_constant__ Params p) {
+template <int BITS, int RB_>
+__global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(const __grid_constant__ Params p) {
+  using C = PfCfg<RB_>;
+  constexpr int RB = C::RB, NST = C::NST, kDecW = C::kDecW, kProdW = C::kProdW, kMmaW = C::kMmaW;
+  constexpr uint32_t STAGE = C::STAGE;
   extern __shared__ __align__(1024) uint8_t smem[];
   const Geo& g = p.g;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -144,7 +153,8 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_c
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kProdW) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(C::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -423,10 +433,13 @@ __global__ void __launch_bounds__(kThreads, 1) owq_prefill_kernel(const __grid_c
   __syncthreads();
   if (warp == kProdW) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::kTmemCols));
   }
   if (threadIdx.x == 0) PF_CTA(3);
 }
+
+template <int RB>
+static owq_status launch_rb(Params& p, const Geo& g, int B, cudaStream_t stream);
 
 owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, cudaStream_t stream) {
   Params p{};
@@ -458,12 +471,29 @@ owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return OWQ_ERR_CUDA;
   }
-  auto kern = g.bits == 3 ? owq_prefill_kernel<3> : owq_prefill_kernel<4>;
+  // Row-blocks per CTA: waves x per-CTA time, a one-row-block CTA taking ~0.6 of
+  // a two-row-block one (half the decode and MMAs, the same x tile)
+  int dev0 = 0, nsm = 148;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev0);
+  const int64_t tiles = (B + NT - 1) / NT, sms = nsm;
+  const int64_t w2 = (tiles * ((g.nrb + 1) / 2) + sms - 1) / sms, w1 = (tiles * g.nrb + sms - 1) / sms;
+  int rbsel = 6 * w1 < 10 * w2 ? 1 : 2;
+#ifdef OWQ_EXPERIMENTS
+  if (const char* v = getenv("OWQ_PF_RB")) rbsel = atoi(v) == 1 ? 1 : 2;
+#endif
+  return rbsel == 1 ? launch_rb<1>(p, g, B, stream) : launch_rb<2>(p, g, B, stream);
+}
+
+template <int RB>
+static owq_status launch_rb(Params& p, const Geo& g, int B, cudaStream_t stream) {
+  using C = PfCfg<RB>;
+  auto kern = g.bits == 3 ? owq_prefill_kernel<3, RB> : owq_prefill_kernel<4, RB>;
   int dev = 0;
   cudaGetDevice(&dev);
   static bool configured[2][16] = {};
   if (!configured[g.bits == 3][dev & 15]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem) != cudaSuccess)
       return OWQ_ERR_CUDA;
     configured[g.bits == 3][dev & 15] = true;
   }
@@ -472,8 +502,8 @@ owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3((unsigned)((B + NT - 1) / NT), (unsigned)((g.nrb + RB - 1) / RB));
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmem;
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
