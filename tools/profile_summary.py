@@ -28,6 +28,7 @@ SHAPES = {
     "cc_q": (12288, 12288, 3, 0, 15, 1), "cc_g128": (12288, 12288, 4, 128, 15, 1),
     "sb_llama_up_b8": (11008, 4096, 4, 128, 1, 8), "prefill": (12288, 12288, 3, 0, 15, 2048),
     "sb_llama_up_b8_v2": (11008, 4096, 4, 128, 1, 8), "prefill_v2": (12288, 12288, 3, 0, 15, 2048),
+    "prefill_v3": (12288, 12288, 3, 0, 15, 2048),
 }
 
 
