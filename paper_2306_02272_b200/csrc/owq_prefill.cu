@@ -530,6 +530,13 @@ static owq_status launch_rb(Params& p, const Geo& g, int B, cudaStream_t stream)
 // ============================================================================
 namespace sb {
 
+// experiment builds only: OWQ_SB_SKIP switches roles' work off (timing); the
+// product kernel has the skip mask folded to zero at compile time
+#ifdef OWQ_EXPERIMENTS
+#define SB_SKIP(m) (p.skip & (m))
+#else
+#define SB_SKIP(m) 0
+#endif
 #ifdef OWQ_EXPERIMENTS
 // per-stage clock64 stamps of CTA (0, 0): [event][stage], events 0 producer after
 // empty, 1 decode after full, 2 decode arrive afull, 3 MMA after afull, 4 MMA after
@@ -657,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, OWQ_SB_MINB) owq_gemm_sb_kernel(cons
         if (l >= NST) sb_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
         SB_TR(0, l);
         const uint32_t bytes = ssb * (uint32_t)nsub(l);   // consecutive super-steps are contiguous in the blob
-        if (p.skip & 8) {
+        if (SB_SKIP(8)) {
           mbar_arrive(&full[s]);
           continue;
         }
@@ -682,15 +689,15 @@ __global__ void __launch_bounds__(kThreads, OWQ_SB_MINB) owq_gemm_sb_kernel(cons
       if (lane == 0) sb_wait(&afull[s], ph);   // A decoded and the x tile landed
       if (lane == 0) SB_TR(3, l);
       if (lane == 0) SB_TR(4, l);
-      if (!(p.skip & 16)) fence_proxy_async();   // the landed cp.async (generic-proxy) writes, before the MMA's async-proxy reads
+      if (!SB_SKIP(16)) fence_proxy_async();   // the landed cp.async (generic-proxy) writes, before the MMA's async-proxy reads
       tc_fence_after();
       if (lane == 0) {
-        const int nu = (p.skip & 2) ? 0 : nsub(l);
+        const int nu = SB_SKIP(2) ? 0 : nsub(l);
         for (int u = 0; u < nu; ++u)
           tc_mma_f16_ss_k64<2 * 2048, 2 * NT * 16>(tmem + (uint32_t)(buf * NT), umma_desc(smem_u32(A(s, u)), 2048, 128),
                                                    umma_desc(smem_u32(Bt(s, u)), NT * 16, 128), idesc,
                                                    (first && u == 0) ? 0u : 1u);
-        if (p.skip & 32) {
+        if (SB_SKIP(32)) {
           mbar_arrive(&empty[s]);
           if (last) mbar_arrive(&dfull[buf]);
         } else {
@@ -733,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, OWQ_SB_MINB) owq_gemm_sb_kernel(cons
       if (lane == 0) sb_wait(&full[s], (uint32_t)(l / NST) & 1u);
       __syncwarp();
       if (threadIdx.x == 0) SB_TR(1, l);
-      if (u < nsub(l) && !(p.skip & 1)) {
+      if (u < nsub(l) && !SB_SKIP(1)) {
         const uint8_t* rec = Cd(s) + (size_t)u * ssb;
         uint32_t w[8], o[16];
 #pragma unroll
@@ -767,7 +774,7 @@ __global__ void __launch_bounds__(kThreads, OWQ_SB_MINB) owq_gemm_sb_kernel(cons
       __syncwarp();
       if (lane == 0) SB_TR(5, l);
 #pragma unroll
-      for (int e = lane; e < ((p.skip & 4) ? 0 : SUB * NT * 8); e += 32) {
+      for (int e = lane; e < (SB_SKIP(4) ? 0 : SUB * NT * 8); e += 32) {
         const int u = e / (NT * 8), e2 = e % (NT * 8);
         const int t = e2 >> 3, kc = e2 & 7;
         const int64_t col = (int64_t)(ss0 + SUB * l + u) * 64 + kc * 8;
