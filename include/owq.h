@@ -222,7 +222,7 @@ owq_status owq_gemm_small_batch(const owq_shape *shape, const void *d_packed,
 
 /* Batched GEMV on tensor cores with an exact fp16 A operand:
  * Y = W_hat X for batch in [1, 32], layout-3 blobs, per-row or grouped scales
- * (group_size a multiple of 64), c_in % 8 == 0, d_x 16-byte aligned.  A = the
+ * (any group_size owq_shape allows), c_in % 8 == 0, d_x 16-byte aligned.  A = the
  * exact integer (q - z) as fp16 in shared memory, B = x (N = batch padded to
  * 16 / 32), fp32 D in TMEM, one D per scale group drained by s_g; K split over
  * the grid with a deterministic last-arriver sum.  Workspace: the GEMV

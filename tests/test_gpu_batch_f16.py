@@ -59,12 +59,30 @@ def test_opt175b_per_row(dev, B):
 
 @pytest.mark.parametrize("M,K,bits,group,k,B", [
     (300, 4000, 3, 0, 11, 5), (130, 640, 4, 128, 3, 7), (257, 1024, 3, 256, 5, 2), (64, 64, 3, 0, 0, 16),
+    (512, 1024, 4, 128, 3, 5), (384, 2048, 3, 128, 4, 32),   # groups of two super-steps, ragged rows, B = 32
 ])
 def test_small_and_ragged(dev, M, K, bits, group, k, B):
     d = synth.representation(M, K, bits, group, k, seed=M + B)
     x = synth.activations(B, K, seed=B, outliers=d["weak_idx"])
     y = run(d, x, dev)
     e, eu = rel_err(y, O.matvec(rep_from_synth(d), x.astype(np.float64)))
+    assert e <= TOL, (e, eu)
+
+
+@pytest.mark.parametrize("B", [4, 9, 16])
+def test_small_batch_routes_grouped(dev, B):
+    """owq_gemm_small_batch with grouped scales at B >= 4 runs this kernel (DESIGN.md
+    §6.5): its result equals owq_gemm_batch_f16's bit for bit and the oracle's within
+    the bound."""
+    M, K, k = 1100, 2048, 3
+    d = synth.representation(M, K, 4, 128, k, seed=40 + B)
+    x = synth.activations(B, K, seed=50 + B, outliers=d["weak_idx"])
+    L = owq.OwqLinear(d, device=dev, layout=owq.OWQ_LAYOUT_TC)
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float16)).to(dev)
+    a = owq.owq_gemm_small_batch(L.shape, L.packed, xt, y_f32=True, ws=L.ws).cpu().numpy()
+    b = owq.owq_gemm_batch_f16(L.shape, L.packed, xt, y_f32=True, ws=L.ws).cpu().numpy()
+    assert np.array_equal(a, b)
+    e, eu = rel_err(a.astype(np.float64), O.matvec(rep_from_synth(d), x.astype(np.float64)))
     assert e <= TOL, (e, eu)
 
 

@@ -58,6 +58,18 @@ def test_prefill_opt175b_sampled(dev, M, K, k):
     assert e <= TOL, (e, eu)
 
 
+def test_prefill_two_rowblock_ctas(dev):
+    """Enough token tiles that the launcher picks two row-blocks per CTA (the
+    x tile shared by two accumulators): 12288 x 4096 at 2048 tokens, sampled rows."""
+    M, K, k, B = 12288, 4096, 6, 2048
+    d = synth.representation(M, K, 3, 0, k, seed=11)
+    x = synth.activations(B, K, seed=12, outliers=d["weak_idx"])
+    y = run(d, x, dev)
+    rows = sorted(set([0, 127, 128, 255, 256, M - 1] + list(np.random.default_rng(3).choice(M, 40, replace=False))))
+    e, eu = rel_err(y[:, rows], O.matvec_rows(rep_from_synth(d), x.astype(np.float64), rows))
+    assert e <= TOL, (e, eu)
+
+
 def test_prefill_fp16_out_and_probes(dev):
     # x = e_j probes: non-weak j -> s (q - z) exactly; weak j -> v exactly (fp32 out)
     M, K, k = 256, 512, 4
