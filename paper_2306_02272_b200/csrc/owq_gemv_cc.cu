@@ -240,6 +240,15 @@ struct XPre {
   __half v[S][NB];        // x[b][column 32 (st + w S + t) + lane]
 };
 
+#ifdef OWQ_EXPERIMENTS
+// per CTA (globaltimer ns): start, x available (after griddepcontrol.wait), main
+// loop done, exit (tools/cc_trace.py)
+__device__ unsigned long long g_cc_cta[4][1024];
+#define CC_STAMP(ev) do { if (threadIdx.x == 0 && blockIdx.x < 1024) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_cc_cta[ev][blockIdx.x] = t_; } } while (0)
+#else
+#define CC_STAMP(ev) do { } while (0)
+#endif
 template <int BITS, int NB>
 __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) owq_gemv_cc_kernel(const Params p) {
   using C = Cfg<BITS, NB>;
@@ -269,6 +278,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  CC_STAMP(0);
   if (u1 <= u0) return;
   const uint32_t ring0 = smem_u32(smem);
 
@@ -318,6 +328,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
   const int c_first = first_partial ? cta_of(rb_first * n_rb) : cta;
 
   pdl_wait();   // x, y and the workspace belong to earlier kernels until they complete
+  CC_STAMP(1);
 
   float tot[NB][4];
   float2 acc[NB][4][2];     // two FFMA2 chains per row (even / odd column pairs)
@@ -589,6 +600,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
     if (!wk.next_rb()) break;
   }
 
+  CC_STAMP(2);
   // ---------------------------------------------------- summer: wait for the lower pieces
   if (have_keep && threadIdx.x < kRowBlock) {
     const int row = threadIdx.x;
@@ -619,6 +631,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NB>::THREADS, Cfg<BITS, NB>::MINB) o
         else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(o);
       }
   }
+  CC_STAMP(3);
 }
 
 // Device inverse of layout 4 (test hook): one thread per (row, column).
@@ -747,3 +760,9 @@ owq_status unpack(const Geo& g, const void* blob, uint8_t* codes, cudaStream_t s
 
 }  // namespace cc
 }  // namespace owq
+
+#ifdef OWQ_EXPERIMENTS
+extern "C" int owq_exp_cc_cta(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, owq::cc::g_cc_cta, sizeof(owq::cc::g_cc_cta));
+}
+#endif
