@@ -687,6 +687,9 @@ static owq_status launch_t(Params& p, cudaStream_t stream) {
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+#ifdef OWQ_EXPERIMENTS
+  if (const char* v = getenv("OWQ_CC_PDL")) attr[0].val.programmaticStreamSerializationAllowed = atoi(v) ? 1 : 0;
+#endif
   cfg.gridDim = dim3((unsigned)p.grid);
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
