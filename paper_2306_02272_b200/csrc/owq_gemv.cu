@@ -1628,7 +1628,30 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
     for (int i = 0; i < cache_n && hit < 0; ++i)
       if (!std::memcmp(cache[i].key, key, sizeof(key))) hit = i;
     if (hit < 0) {
-      for (int64_t c = 0; c <= grid; ++c) p.span[c] = (int32_t)cta_first_item(g, grid, c);
+      // CTA c's share of the bytes ~ 1 + a (1/2 - c/G).  In a chain of calls the
+      // CTAs of a call start as the previous call's CTAs leave their SMs, in CTA
+      // order, over several microseconds, and a late starter has had less time to
+      // fill its ring before x is readable: giving the high
+      // indices less work evens the finish.  a ~ 88 KB / (bytes per CTA), i.e.
+      // ~2 us of one SM's HBM share, capped at 0.3 (measured: 12288^2 -7 %,
+      // 49152 x 12288 -2 %; a reversed skew is slower).
+      const double T = (double)g.nrb * g.rb_bytes;
+      static const int skew_env = knob("OWQ_SKEW", -1);   // experiments: a = OWQ_SKEW / 100
+      const int64_t n_items = (int64_t)g.nrb * items_per_rb(g);
+      // only with >= 8 items per CTA; spans stay non-empty (the fixup's summer
+      // waits on every CTA between a row-block's first and last piece)
+      const double a = n_items < 8 * grid ? 0.0
+                       : skew_env >= 0 ? skew_env / 100.0 : std::min(0.3, 88.0 * 1024.0 * grid / T);
+      if (a <= 0.0) {
+        for (int64_t c = 0; c <= grid; ++c) p.span[c] = (int32_t)cta_first_item(g, grid, c);
+      } else {
+        for (int64_t c = 0; c <= grid; ++c) {
+          const double xx = (double)c / grid, F = xx + 0.5 * a * (xx - xx * xx);
+          p.span[c] = c == grid ? (int32_t)cta_first_item(g, grid, c) : (int32_t)first_item_at(g, (int64_t)std::ceil(T * F));
+        }
+        for (int64_t c = 1; c < grid; ++c) p.span[c] = std::max(p.span[c], p.span[c - 1] + 1);
+        for (int64_t c = grid - 1; c >= 1; --c) p.span[c] = std::min(p.span[c], p.span[c + 1] - 1);
+      }
       {  // row-block pieces at each CTA's ends (the fixup's summer and piece count)
         const int64_t n_rb = items_per_rb(g);
         auto cta_of = [&](int64_t item) {   // span[c] <= item < span[c + 1]
