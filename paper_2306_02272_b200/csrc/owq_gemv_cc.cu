@@ -727,6 +727,19 @@ owq_status gemm(const Geo& g, const void* blob, const uint16_t* x, int B, void* 
     const int64_t T = (int64_t)g.nrb * rb_bytes(g);
     for (int c = 0; c <= grid; ++c)
       cache[hit].span[c] = (int32_t)first_unit_at(g, cdiv((int64_t)c * T, grid));
+    double a = 0.0;   // span skew toward early CTAs (owq_gemv.cu); experiments only so far
+#ifdef OWQ_EXPERIMENTS
+    if (const char* v = getenv("OWQ_CC_SKEW")) a = atoi(v) / 100.0;
+#endif
+    if (a > 0.0 && cache[hit].span[grid] >= 8 * (int64_t)grid) {
+      int32_t* sp = cache[hit].span;
+      for (int c = 1; c < grid; ++c) {
+        const double xx = (double)c / grid, F = xx + 0.5 * a * (xx - xx * xx);
+        sp[c] = (int32_t)first_unit_at(g, (int64_t)std::ceil((double)T * F));
+      }
+      for (int c = 1; c < grid; ++c) sp[c] = std::max(sp[c], sp[c - 1] + 1);
+      for (int c = grid - 1; c >= 1; --c) sp[c] = std::min(sp[c], sp[c + 1] - 1);
+    }
     for (int i = 0; i < 3; ++i) cache[hit].key[i] = key[i];
   }
   std::copy(cache[hit].span, cache[hit].span + grid + 1, p.span);
