@@ -243,6 +243,22 @@ owq_status owq_gemm_prefill(const owq_shape *shape, const void *d_packed,
                             const uint16_t *d_x, int32_t n_tokens, void *d_y,
                             int y_f32, void *stream);
 
+/* Prefill with a scratch workspace (16-byte aligned, any contents, at least
+ * owq_prefill_workspace_bytes()): the K loop is split into pieces of at most 64
+ * super-steps (4096 columns; the tensor core's fp32 accumulation over longer
+ * loops exceeds the 2e-3 bound) and, when even one-row-block
+ * CTAs would fill at most half the SMs, into up to 8 pieces; each piece stores
+ * fp32 partial rows in the workspace and a second kernel adds them in piece
+ * order (deterministic).  owq_gemm_prefill (no workspace) returns
+ * OWQ_ERR_BUFFER_TOO_SMALL whenever a split is needed, i.e. c_in > 4096. */
+owq_status owq_gemm_prefill_ws(const owq_shape *shape, const void *d_packed,
+                               const uint16_t *d_x, int32_t n_tokens, void *d_y,
+                               int y_f32, void *d_workspace, size_t ws_bytes,
+                               void *stream);
+/* Workspace bytes owq_gemm_prefill_ws needs at n_tokens on the current device
+ * (0 = no split, owq_gemm_prefill suffices; 0 also for an invalid shape). */
+size_t owq_prefill_workspace_bytes(const owq_shape *shape, int32_t n_tokens);
+
 /* Test/tuning hook: same as owq_gemm_small_batch with an explicit grid size
  * (number of CTAs; 0 = one per SM; capped at one CTA per item; > 512 after the
  * cap -> UNSUPPORTED).  Small grids exercise the stream-K partial-sum path with

@@ -29,7 +29,7 @@ __all__ = [
     "owq_packed_bytes_layout", "owq_workspace_bytes_grid", "owq_packed_bytes_colmap", "owq_pack_host_colmap",
     "owq_pack_colmap", "owq_blob_colmap_host", "choose_layout", "owq_quantize_gpu",
     "owq_quantize_workspace_bytes", "owq_gemm_prefill", "owq_gemm_batch_f16", "owq_tp_check",
-    "EXPORTED_SYMBOLS",
+    "owq_prefill_workspace_bytes", "prefill_workspace", "EXPORTED_SYMBOLS",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -48,7 +48,7 @@ EXPORTED_SYMBOLS = [
     "owq_tp_gemv", "owq_tp_bounds", "owq_status_string", "owq_packed_bytes_colmap",
     "owq_pack_host_colmap", "owq_pack_colmap", "owq_blob_colmap_host",
     "owq_quantize_workspace_bytes", "owq_quantize_gpu", "owq_gemm_prefill", "owq_gemm_batch_f16",
-    "owq_tp_check",
+    "owq_tp_check", "owq_gemm_prefill_ws", "owq_prefill_workspace_bytes",
 ]
 
 
@@ -132,6 +132,8 @@ def lib():
         "owq_pack_colmap": (st, [_S, ctypes.POINTER(_HostLayer), ctypes.POINTER(_ColMap), ctypes.c_int, _P, sz, _P]),
         "owq_blob_colmap_host": (st, [_P, sz, ctypes.POINTER(ctypes.c_int32), _P]),
         "owq_gemm_prefill": (st, [_S, _P, _P, ctypes.c_int32, _P, ctypes.c_int, _P]),
+        "owq_gemm_prefill_ws": (st, [_S, _P, _P, ctypes.c_int32, _P, ctypes.c_int, _P, sz, _P]),
+        "owq_prefill_workspace_bytes": (sz, [_S, ctypes.c_int32]),
         "owq_gemm_batch_f16": (st, [_S, _P, _P, ctypes.c_int, _P, ctypes.c_int, _P, sz, _P]),
         "owq_quantize_workspace_bytes": (sz, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                               ctypes.POINTER(_QuantParams)]),
@@ -432,16 +434,41 @@ def owq_gemm_batch_f16(shape, d_packed, x, y=None, y_f32=False, ws=None, stream=
     return y
 
 
-def owq_gemm_prefill(shape, d_packed, x, y=None, y_f32=False, stream=None):
+def owq_prefill_workspace_bytes(shape, n_tokens: int) -> int:
+    return int(lib().owq_prefill_workspace_bytes(ctypes.byref(_shape(shape)), int(n_tokens)))
+
+
+def prefill_workspace(shape, n_tokens: int, device=None):
+    """Scratch workspace for owq_gemm_prefill(..., ws=...) (K-split partial rows),
+    or None when no split would be used at this token count."""
+    import torch
+    dev = torch.device(device or "cuda")
+    with torch.cuda.device(dev):
+        n = owq_prefill_workspace_bytes(shape, n_tokens)
+    return torch.empty(n, dtype=torch.uint8, device=dev) if n else None
+
+
+def owq_gemm_prefill(shape, d_packed, x, y=None, y_f32=False, ws=None, stream=None):
     """Y = W_hat X for fp16 X [n_tokens][c_in], any n_tokens (NEXT-2, tensor cores,
-    layout-3 blobs with per-row scales); returns Y [n_tokens][c_out]."""
+    layout-3 blobs with per-row scales); returns Y [n_tokens][c_out].  K is split
+    into pieces of <= 4096 columns (precision) and, for few tokens on few rows,
+    over more CTAs; the scratch comes from `ws` (prefill_workspace) or is
+    allocated per call."""
     s = _shape(shape)
     B = x.shape[0] if x.dim() == 2 else 1
     y = _out(s, B, y, y_f32, x.device)
     _check_io(s, d_packed, x, y, y_f32, B, None)
     with _on_device(d_packed.device):
-        _check(lib().owq_gemm_prefill(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B, y.data_ptr(),
-                                      int(bool(y_f32)), _stream(stream)))
+        if ws is None:
+            ws = prefill_workspace(s, B, x.device)   # None when K needs no split
+        if ws is None:
+            _check(lib().owq_gemm_prefill(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B, y.data_ptr(),
+                                          int(bool(y_f32)), _stream(stream)))
+        else:
+            if ws.device != x.device or ws.dtype.itemsize != 1 or not ws.is_contiguous():
+                raise OwqError("OWQ_ERR_INVALID_ARG: prefill workspace must be a contiguous byte tensor on x's device")
+            _check(lib().owq_gemm_prefill_ws(ctypes.byref(s), d_packed.data_ptr(), x.data_ptr(), B, y.data_ptr(),
+                                             int(bool(y_f32)), ws.data_ptr(), ws.numel(), _stream(stream)))
     return y
 
 

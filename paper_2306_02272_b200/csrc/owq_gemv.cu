@@ -56,7 +56,9 @@ int grid_for(const Geo& g, int grid_req);
 size_t workspace_bytes(int grid, int nb);
 }  // namespace cc
 namespace pf {   // owq_prefill.cu
-owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, cudaStream_t stream);
+owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, void* ws,
+                  size_t ws_bytes, cudaStream_t stream);
+size_t workspace_bytes(const Geo& g, int B);
 namespace sb {
 owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, void* ws,
                   size_t ws_bytes, int sms, cudaStream_t stream);
@@ -1847,8 +1849,8 @@ owq_status owq_gemm_batch_f16(const owq_shape* s, const void* d_packed, const ui
                         (uint8_t*)d_ws + ws_sync(), ws_bytes - ws_sync(), device_sms(), (cudaStream_t)stream);
 }
 
-owq_status owq_gemm_prefill(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int32_t n_tokens, void* d_y,
-                            int y_f32, void* stream) {
+static owq_status prefill_impl(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int32_t n_tokens,
+                               void* d_y, int y_f32, void* d_ws, size_t ws_bytes, void* stream) {
   if (!d_x || !d_y) return OWQ_ERR_INVALID_ARG;
   if (n_tokens < 1) return OWQ_ERR_INVALID_ARG;
   int layout = 0, Ks = -1;
@@ -1856,8 +1858,25 @@ owq_status owq_gemm_prefill(const owq_shape* s, const void* d_packed, const uint
   if (st != OWQ_OK) return st;
   if (layout != OWQ_LAYOUT_VERSION || s->group_size != 0 || (s->c_in & 7)) return OWQ_ERR_UNSUPPORTED;
   if (reinterpret_cast<uintptr_t>(d_x) & 15) return OWQ_ERR_INVALID_ARG;
+  if (d_ws && (reinterpret_cast<uintptr_t>(d_ws) & 15)) return OWQ_ERR_INVALID_ARG;
   return pf::launch(make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak), d_packed, d_x, n_tokens, d_y, y_f32,
-                    (cudaStream_t)stream);
+                    d_ws, d_ws ? ws_bytes : 0, (cudaStream_t)stream);
+}
+
+owq_status owq_gemm_prefill(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int32_t n_tokens, void* d_y,
+                            int y_f32, void* stream) {
+  return prefill_impl(s, d_packed, d_x, n_tokens, d_y, y_f32, nullptr, 0, stream);
+}
+
+owq_status owq_gemm_prefill_ws(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int32_t n_tokens,
+                               void* d_y, int y_f32, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!d_ws && ws_bytes) return OWQ_ERR_INVALID_ARG;
+  return prefill_impl(s, d_packed, d_x, n_tokens, d_y, y_f32, d_ws, ws_bytes, stream);
+}
+
+size_t owq_prefill_workspace_bytes(const owq_shape* s, int32_t n_tokens) {
+  if (owq_packed_bytes(s) == 0 || n_tokens < 1) return 0;
+  return pf::workspace_bytes(make_geo(s->c_out, s->c_in, s->bits, s->group_size, s->n_weak), n_tokens);
 }
 
 owq_status owq_gemm_small_batch_grid(const owq_shape* s, const void* d_packed, const uint16_t* d_x, int batch,

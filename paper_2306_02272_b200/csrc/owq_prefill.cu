@@ -73,6 +73,8 @@ struct Params {
   void* y;             // [B][M]
   Geo g;
   int32_t B, y_f32;
+  int32_t KS, sps;     // K splits and super-steps per split (KS = 1: no split)
+  float* part;         // KS > 1: [KS][B][Mp] fp32 partial rows (Mp = nrb x 128), summed by owq_prefill_reduce_kernel
 };
 
 // one row's 64 codes of a super-step -> 16 words of 4 code bytes (layout 3)
@@ -130,6 +132,8 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x, rb0 = blockIdx.y * RB;
   const int nss = g.nss;
+  const int split = blockIdx.z;                                      // K split (p.KS > 1, prefill with a workspace)
+  const int ss0 = split * p.sps, nl = min(nss, ss0 + p.sps) - ss0;   // this CTA's super-steps
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + NST * STAGE);
   uint64_t* full = bars;               // codes landed (TMA tx)
@@ -168,9 +172,10 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
     // ------------------------------------------------ producer: codes of each super-step (TMA bulk)
     if (lane == 0) {
       pdl_launch_dependents();
-      for (int ss = 0; ss < nss; ++ss) {
-        const int s = ss % NST;
-        if (ss >= NST) mbar_wait(&empty[s], (uint32_t)((ss / NST) - 1) & 1u);
+      for (int l = 0; l < nl; ++l) {
+        const int ss = ss0 + l;
+        const int s = l % NST;
+        if (l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
         PF_TR(0, ss);
         mbar_expect_tx(&full[s], ssb * nrb_here);
         for (int h = 0; h < nrb_here; ++h)
@@ -181,9 +186,10 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
     // ------------------------------------------------ MMA issue (one thread): per row-block h,
     // D_h (TMEM columns 256 h ..) += A_h x B
     constexpr uint32_t idesc = idesc_f16(128, NT);
-    for (int ss = 0; ss < nss; ++ss) {
-      const int s = ss % NST;
-      const uint32_t ph = (uint32_t)(ss / NST) & 1u;
+    for (int l = 0; l < nl; ++l) {
+        const int ss = ss0 + l;
+      const int s = l % NST;
+      const uint32_t ph = (uint32_t)(l / NST) & 1u;
       mbar_wait(&afull[s], ph);
       if (lane == 0) PF_TR(3, ss);
       mbar_wait(&bfull[s], ph);
@@ -196,10 +202,10 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)   // K = 16 per MMA: A two 8-element core-matrix columns, B 32 bytes into each swizzled row
             tc_mma_f16_ss(tmem + (uint32_t)(h * NT), umma_desc(a0 + kk * 2 * 2048, 2048, 128),
-                          umma_desc_sw128(b0 + kk * 32), idesc, (ss | kk) != 0 ? 1u : 0u);
+                          umma_desc_sw128(b0 + kk * 32), idesc, (l | kk) != 0 ? 1u : 0u);
         }
         tc_commit(&empty[s]);
-        if (ss == nss - 1) tc_commit(dfull);
+        if (l == nl - 1) tc_commit(dfull);
       }
       __syncwarp();
     }
@@ -214,9 +220,10 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
     const __half2 zz = __float2half2_rn(1024.f + z);   // exact: z <= 15
     const uint32_t zzw = *reinterpret_cast<const uint32_t*>(&zz);
     constexpr int WPR = BITS == 3 ? 6 : 8;
-    for (int ss = 0; ss < nss; ++ss) {
-      const int s = ss % NST;
-      mbar_wait(&full[s], (uint32_t)(ss / NST) & 1u);
+    for (int l = 0; l < nl; ++l) {
+        const int ss = ss0 + l;
+      const int s = l % NST;
+      mbar_wait(&full[s], (uint32_t)(l / NST) & 1u);
       if (threadIdx.x == 0) PF_TR(1, ss);
       if (!live) {          // the CTA's second row-block does not exist: nothing to decode
         mbar_arrive(&afull[s]);
@@ -265,7 +272,7 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
     tc_fence_after();
     const uint16_t* widx = reinterpret_cast<const uint16_t*>(p.blob + g.widx_off);
     const uint8_t* wrec = p.blob + g.units_off + (int64_t)rb * g.rb_bytes + (int64_t)g.nss * g.ss_bytes;
-    const int k = g.k;
+    const int k = split == 0 ? g.k : 0;   // the weak fold goes into the first K split only
     auto wval = [&](int tt) {
       const int ch = tt / kWeakChunk, c = tt % kWeakChunk;
       return ch < g.nfull ? *reinterpret_cast<const __half*>(wrec + (int64_t)ch * kWeakChunkBytes + (r * kWeakChunk + c) * 2)
@@ -325,7 +332,7 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
     // writing 2-byte elements of 32 rows per token measured ~4000 cycles per pass).
     const int ysz = p.y_f32 ? 4 : 2;
     uint8_t* ystage = base + wis_bytes + xw_bytes + (wstaged ? (((size_t)RB * k * 256 + 127) & ~(size_t)127) : 0);
-    const bool ystaged = (size_t)(ystage - base) + (size_t)32 * RB * 128 * ysz <= ring;
+    const bool ystaged = p.KS == 1 && (size_t)(ystage - base) + (size_t)32 * RB * 128 * ysz <= ring;
     const int rows_here = nrb_here * 128;
     for (int c16 = 0; c16 < NT / 16; c16 += 2) {
       if (!xall) {
@@ -366,7 +373,15 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
             }
           }
         }
-        if (ystaged) {
+        if (p.KS > 1) {
+          // K split: this split's fp32 partial rows (owq_prefill_reduce_kernel sums them)
+          const int64_t Mp = (int64_t)g.nrb * kRowBlock;
+#pragma unroll
+          for (int jj = 0; jj < 32; ++jj) {
+            const int64_t n = tok0 + c16 * 16 + jj;
+            if (n < p.B) __stcg(&p.part[((int64_t)split * p.B + n) * Mp + grow], v[jj]);
+          }
+        } else if (ystaged) {
           // ystage[token j][row h*128 + r]
 #pragma unroll
           for (int jj = 0; jj < 32; ++jj) {
@@ -419,9 +434,10 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
     if (lane == 0) {
       pdl_wait();   // x belongs to earlier kernels until they complete
       PF_CTA(1);
-      for (int ss = 0; ss < nss; ++ss) {
-        const int s = ss % NST;
-        if (ss >= NST) mbar_wait(&empty[s], (uint32_t)((ss / NST) - 1) & 1u);
+      for (int l = 0; l < nl; ++l) {
+        const int ss = ss0 + l;
+        const int s = l % NST;
+        if (l >= NST) mbar_wait(&empty[s], (uint32_t)((l / NST) - 1) & 1u);
         PF_TR(5, ss);
         mbar_expect_tx(&bfull[s], B_BYTES);
         tma_load_2d(Bt(s), &p.xmap, ss * 64, (int)tok0, &bfull[s]);
@@ -441,7 +457,70 @@ __global__ void __launch_bounds__(PfCfg<RB_>::kThreads, 1) owq_prefill_kernel(co
 template <int RB>
 static owq_status launch_rb(Params& p, const Geo& g, int B, cudaStream_t stream);
 
-owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, cudaStream_t stream) {
+// y[n][row] = sum over the K splits, in split order, of the fp32 partial rows
+// (four rows per thread)
+__global__ void owq_prefill_reduce_kernel(const float* __restrict__ part, int KS, int B, int64_t M, int64_t Mp,
+                                          void* y, int y_f32) {
+  pdl_wait();   // the partials come from the prefill kernel just before
+  const int64_t q4 = (M + 3) / 4;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * q4) return;
+  const int64_t n = i / q4, row = (i - n * q4) * 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int sp = 0; sp < KS; ++sp) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(part + ((int64_t)sp * B + n) * Mp + row));
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  const float vv[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if (row + e >= M) break;
+    if (y_f32) reinterpret_cast<float*>(y)[n * M + row + e] = vv[e];
+    else reinterpret_cast<__half*>(y)[n * M + row + e] = __float2half_rn(vv[e]);
+  }
+}
+
+// Row-blocks per CTA (waves x per-CTA time, a one-row-block CTA taking ~0.6 of a
+// two-row-block one: half the decode and MMAs, the same x tile) and K splits.
+// Precision: the tensor core's fp32 accumulation over a long K loop is not
+// round-to-nearest per add -- one TMEM accumulator over 192 super-steps (K =
+// 12288) already exceeds the 2e-3 bound on near-zero outputs, K = 49152 reaches
+// 1.3e-2 (tools/pf_precision.py) -- so every split is at most kPfChain
+// super-steps and the splits are added in fp32 on CUDA cores in split order.
+// Fill: when even one-row-block CTAs would fill at most half the SMs, more
+// splits (up to 8, >= 4 super-steps each).
+constexpr int kPfChain = 64;
+struct PfPlan { int rb, ks, sps; };
+static int pf_sms() {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return nsm;
+}
+static PfPlan pf_plan(const Geo& g, int B, int sms) {
+  const int64_t tiles = (B + NT - 1) / NT;
+  const int64_t w2 = (tiles * ((g.nrb + 1) / 2) + sms - 1) / sms, w1 = (tiles * g.nrb + sms - 1) / sms;
+  PfPlan pl{6 * w1 < 10 * w2 ? 1 : 2, 1, g.nss};
+  int ks = (g.nss + kPfChain - 1) / kPfChain;                       // precision
+  const int64_t ctas1 = tiles * g.nrb;
+  if (2 * ctas1 <= sms) {                                            // fill
+    int kf = (int)std::min<int64_t>(8, sms / ctas1);
+    while (kf > 1 && (g.nss + kf - 1) / kf < 4) --kf;
+    if (kf > ks) { ks = kf; pl.rb = 1; }
+  }
+  if (ks > 1) {
+    pl.sps = (g.nss + ks - 1) / ks;
+    pl.ks = (g.nss + pl.sps - 1) / pl.sps;
+  }
+  return pl;
+}
+size_t workspace_bytes(const Geo& g, int B) {
+  const PfPlan pl = pf_plan(g, B, pf_sms());
+  return pl.ks > 1 ? (size_t)pl.ks * B * g.nrb * kRowBlock * 4 : 0;
+}
+
+owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void* y, int y_f32, void* ws,
+                  size_t ws_bytes, cudaStream_t stream) {
   Params p{};
   p.blob = (const uint8_t*)blob;
   p.x = (const __half*)x;
@@ -471,18 +550,36 @@ owq_status launch(const Geo& g, const void* blob, const uint16_t* x, int B, void
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return OWQ_ERR_CUDA;
   }
-  // Row-blocks per CTA: waves x per-CTA time, a one-row-block CTA taking ~0.6 of
-  // a two-row-block one (half the decode and MMAs, the same x tile)
-  int dev0 = 0, nsm = 148;
-  cudaGetDevice(&dev0);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev0);
-  const int64_t tiles = (B + NT - 1) / NT, sms = nsm;
-  const int64_t w2 = (tiles * ((g.nrb + 1) / 2) + sms - 1) / sms, w1 = (tiles * g.nrb + sms - 1) / sms;
-  int rbsel = 6 * w1 < 10 * w2 ? 1 : 2;
+  PfPlan pl = pf_plan(g, B, pf_sms());
+  if (pl.ks > 1 && (!ws || ws_bytes < (size_t)pl.ks * B * g.nrb * kRowBlock * 4))
+    return OWQ_ERR_BUFFER_TOO_SMALL;   // the K split needs owq_prefill_workspace_bytes() of scratch
 #ifdef OWQ_EXPERIMENTS
-  if (const char* v = getenv("OWQ_PF_RB")) rbsel = atoi(v) == 1 ? 1 : 2;
+  if (const char* v = getenv("OWQ_PF_RB")) pl.rb = atoi(v) == 1 ? 1 : 2;
 #endif
-  return rbsel == 1 ? launch_rb<1>(p, g, B, stream) : launch_rb<2>(p, g, B, stream);
+  p.KS = pl.ks;
+  p.sps = pl.sps;
+  p.part = pl.ks > 1 ? (float*)ws : nullptr;
+  const owq_status st = pl.rb == 1 ? launch_rb<1>(p, g, B, stream) : launch_rb<2>(p, g, B, stream);
+  if (st != OWQ_OK || pl.ks == 1) return st;
+  // the deterministic sum of the splits (PDL: launches while the prefill drains)
+  const int64_t q4 = (g.M + 3) / 4, n = (int64_t)B * q4;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)((n + 255) / 256));
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, owq_prefill_reduce_kernel, (const float*)p.part, pl.ks, B, (int64_t)g.M,
+                     (int64_t)g.nrb * kRowBlock, y, y_f32 ? 1 : 0);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "owq: launch of owq_prefill_reduce_kernel failed: %s\n", cudaGetErrorString(e));
+    return OWQ_ERR_CUDA;
+  }
+  return OWQ_OK;
 }
 
 template <int RB>
@@ -501,7 +598,7 @@ static owq_status launch_rb(Params& p, const Geo& g, int B, cudaStream_t stream)
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.gridDim = dim3((unsigned)((B + NT - 1) / NT), (unsigned)((g.nrb + RB - 1) / RB));
+  cfg.gridDim = dim3((unsigned)((B + NT - 1) / NT), (unsigned)((g.nrb + RB - 1) / RB), (unsigned)p.KS);
   cfg.blockDim = dim3(C::kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = stream;

@@ -91,3 +91,55 @@ def test_prefill_unsupported(dev):
     x = torch.zeros((32, 256), dtype=torch.float16, device=dev)
     with pytest.raises(owq.OwqError, match="UNSUPPORTED"):
         owq.owq_gemm_prefill(L.shape, L.packed, x)
+
+
+@pytest.mark.parametrize("M,K,bits,k,B", [
+    (4096, 4096, 3, 5, 256), (256, 4096, 3, 300, 40), (1000, 2048, 4, 0, 256), (130, 640, 3, 9, 17),
+    (4096, 11008, 4, 4, 128),
+])
+def test_prefill_ksplit_workspace(dev, M, K, bits, k, B):
+    """owq_gemm_prefill with a workspace: few token tiles x row-blocks split K over
+    more CTAs (fp32 partials, a second kernel adds them in split order).  Parity
+    with the oracle, bit-identical repeats, and the no-workspace call within the
+    same bound."""
+    d = synth.representation(M, K, bits, 0, k, seed=M + K + B + 1)
+    x = synth.activations(B, K, seed=B + 1, outliers=d["weak_idx"])
+    L = owq.OwqLinear(d, device=dev, layout=owq.OWQ_LAYOUT_TC)
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float16)).to(dev)
+    ws = owq.prefill_workspace(L.shape, B, dev)
+    assert ws is not None and ws.numel() > 0   # these shapes split
+    ys = []
+    for _ in range(3):
+        y = owq.owq_gemm_prefill(L.shape, L.packed, xt, y_f32=True, ws=ws)
+        torch.cuda.synchronize()
+        ys.append(y.cpu().numpy().astype(np.float64))
+    rep = rep_from_synth(d)
+    y0 = owq.owq_gemm_prefill(L.shape, L.packed, xt, y_f32=True).cpu().numpy().astype(np.float64)
+    y16 = owq.owq_gemm_prefill(L.shape, L.packed, xt, y_f32=False, ws=ws).float().cpu().numpy().astype(np.float64)
+    if M * B <= 1 << 20:
+        rows = slice(None)
+        ref = O.matvec(rep, x.astype(np.float64))
+    else:
+        rows = sorted(set([0, 127, 128, M - 1] + list(np.random.default_rng(2).choice(M, 60, replace=False))))
+        ref = O.matvec_rows(rep, x.astype(np.float64), rows)
+    for name, yy in (("split", ys[0]), ("no split", y0), ("split, fp16 out", y16)):
+        e, eu = rel_err(yy[:, rows], ref)
+        assert e <= TOL, (name, e, eu)
+    assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
+
+
+@pytest.mark.parametrize("bits,K", [(3, 49152), (4, 16384), (3, 12288)])
+def test_prefill_long_k_precision(dev, bits, K):
+    """Long K loops: one fp32 TMEM accumulator over K = 12288 .. 49152 exceeded the
+    2e-3 bound (tools/pf_precision.py: 2.3e-3 .. 1.3e-2); the K pieces of <= 4096
+    columns, added in fp32, stay within it."""
+    M, B = 1024, 128
+    d = synth.representation(M, K, bits, 0, 4, seed=K + bits)
+    x = synth.activations(B, K, seed=7, outliers=d["weak_idx"])
+    L = owq.OwqLinear(d, device=dev, layout=owq.OWQ_LAYOUT_TC)
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float16)).to(dev)
+    assert owq.owq_prefill_workspace_bytes(L.shape, B) > 0
+    y = owq.owq_gemm_prefill(L.shape, L.packed, xt, y_f32=True).cpu().numpy().astype(np.float64)
+    rows = list(range(0, M, 4))
+    e, eu = rel_err(y[:, rows], O.matvec_rows(rep_from_synth(d), x.astype(np.float64), rows))
+    assert e <= TOL, (e, eu)
