@@ -29,6 +29,7 @@ SHAPES = {
     "sb_llama_up_b8": (11008, 4096, 4, 128, 1, 8), "prefill": (12288, 12288, 3, 0, 15, 2048),
     "sb_llama_up_b8_v2": (11008, 4096, 4, 128, 1, 8), "prefill_v2": (12288, 12288, 3, 0, 15, 2048),
     "prefill_v3": (12288, 12288, 3, 0, 15, 2048),
+    "prefill_v4": (12288, 12288, 3, 0, 15, 2048),   # one K piece (64 super-steps) of the split launch
 }
 
 
