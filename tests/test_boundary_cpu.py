@@ -124,3 +124,15 @@ def test_tp_shards_partition_the_layer(mode, world):
         covered += b - a
     assert covered == (M if mode == owq.OWQ_TP_ROWS else K)
     assert np.allclose(acc, y_ref, rtol=1e-12, atol=1e-12)
+
+
+def test_prefill_workspace_sizing():
+    """owq_prefill_workspace_bytes (host logic, no GPU needed): K pieces of at most
+    64 super-steps (4096 columns) are needed whenever c_in > 4096 -- B x c_out(padded
+    to 128) fp32 partial rows per piece -- and none for c_in <= 4096 on a wide layer."""
+    s = owq.Shape(12288, 12288, 3, 0, 15)
+    n = owq.owq_prefill_workspace_bytes(s, 2048)
+    assert n >= 3 * 2048 * 12288 * 4 and n % (2048 * 12288 * 4) == 0
+    assert owq.owq_prefill_workspace_bytes(owq.Shape(12288, 4096, 3, 0, 15), 2048) == 0
+    assert owq.owq_prefill_workspace_bytes(owq.Shape(130, 49152, 4, 0, 3), 17) >= 12 * 17 * 256 * 4
+    assert owq.owq_prefill_workspace_bytes(owq.Shape(0, 4096, 3, 0, 0), 8) == 0   # invalid shape
