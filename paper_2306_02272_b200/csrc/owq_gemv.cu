@@ -1258,7 +1258,47 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
           pieces(crb, c_first, c_last);
           const int npieces = (int)(c_last - c_first + 1);
           uint32_t* pw = p.slots;   // [cta][B][128]: each CTA has at most one non-summer piece (its first row-block)
-          if (p.coresident) {
+#ifndef OWQ_SUMMER_LOW
+#define OWQ_SUMMER_LOW 0   // A/B builds only: 1 = round 1's lowest-piece summer compiled in alone
+#endif
+          if ((OWQ_SUMMER_LOW || (kTrace && p.exp == 7)) && p.coresident) {
+            // A/B only (OWQ_EXP=7 or -DOWQ_SUMMER_LOW=1): round 1's protocol, the lowest
+            // piece sums.  Faster (12288^2: -0.3 us at B = 1, -4..7 us at B = 8..16,
+            // profiles/r2_summer_ab.txt) but its summer waits on HIGHER-index CTAs: two
+            // full grids on concurrent streams (the bench's q/k/v) can each hold SMs
+            // the other's missing pieces need, so it is not the product protocol.
+            if (cta != c_first) {
+#pragma unroll
+              for (int b = 0; b < MAXB; ++b)
+                if (b < p.B) st_relaxed(pw + (cta * p.B + b) * kRowBlock + row, ~__float_as_uint(tot[b]));
+            } else {
+              for (int qq = 1; qq < npieces; ++qq) {
+                uint32_t w[MAXB];
+#pragma unroll
+                for (int b = 0; b < MAXB; ++b)
+                  w[b] = b < p.B ? ld_relaxed(pw + ((c_first + qq) * p.B + b) * kRowBlock + row) : 1u;
+#pragma unroll
+                for (int b = 0; b < MAXB; ++b)
+                  if (b < p.B) {
+                    uint32_t* a = pw + ((c_first + qq) * p.B + b) * kRowBlock + row;
+                    while (w[b] == 0u) {
+                      __nanosleep(32);
+                      w[b] = ld_relaxed(a);
+                    }
+                    st_relaxed(a, 0u);
+                    tot[b] += __uint_as_float(~w[b]);
+                  }
+              }
+              if (grow < g.M) {
+#pragma unroll
+                for (int b = 0; b < MAXB; ++b)
+                  if (b < p.B) {
+                    if (p.y_f32) reinterpret_cast<float*>(p.y)[(int64_t)b * g.M + grow] = tot[b];
+                    else reinterpret_cast<__half*>(p.y)[(int64_t)b * g.M + grow] = __float2half_rn(tot[b]);
+                  }
+              }
+            }
+          } else if (p.coresident) {
             // Fixed summer = the CTA holding the row-block's LAST item (the
             // highest-index piece, CUTLASS's stream-K rule).  For that CTA the
             // row-block is its first one, so it parks its partial in its own
@@ -1320,7 +1360,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       cli = nli;
       cn = nn;
     }
-    if (keep_rb >= 0) {
+    if (!OWQ_SUMMER_LOW && keep_rb >= 0) {
       // summer of its first row-block: add the lower pieces in CTA order, then its own
       int64_t c_first, c_last;
       pieces(keep_rb, c_first, c_last);
@@ -1330,6 +1370,7 @@ __global__ void __launch_bounds__(Cfg<BITS, NN, DWG_, GRP>::kThreads, 1) owq_gem
       for (int b = 0; b < MAXB; ++b) v[b] = 0.f;
       for (int64_t c = c_first; c < c_last; ++c) {
         // all batch rows of piece c in flight at once, then wait for the late ones
+        // (one row at a time costs a round trip per row: +3 us at B = 8)
         uint32_t w[MAXB];
 #pragma unroll
         for (int b = 0; b < MAXB; ++b) w[b] = b < p.B ? ld_relaxed(pw + (c * p.B + b) * kRowBlock + row) : 1u;
@@ -1684,6 +1725,8 @@ static owq_status gemm_impl(const owq_shape* s, const void* d_packed, const uint
     }
   }
   p.coresident = grid <= device_sms() ? 1 : 0;   // one CTA per SM: every CTA is resident at once
+  static const int force_counter = knob("OWQ_FORCE_COUNTER", 0);   // experiments: the counter fixup for every grid
+  if (force_counter) p.coresident = 0;
   p.B = B;
   p.Bp = batch_pad(B);
   p.y_f32 = y_f32 ? 1 : 0;
