@@ -316,6 +316,33 @@ def test_concurrent_full_grids(dev, layout):
         assert e <= TOL
 
 
+@pytest.mark.timeout(300)
+def test_concurrent_full_grids_batched(dev):
+    """As above at B = 8 on the tcgen05 kernel (MMA N = 48, eight batch rows per
+    fixup slot): two full grids compete for the SMs; every call completes and
+    matches the oracle."""
+    cases = [(12288, 4096, 3, 0, 15), (8192, 6144, 3, 0, 9)]
+    B = 8
+    streams = [torch.cuda.Stream() for _ in cases]
+    runs = []
+    for i, (M, K, bits, g, k) in enumerate(cases):
+        d = synth.representation(M, K, bits, g, k, seed=700 + i)
+        x = synth.activations(B, K, seed=800 + i, outliers=d["weak_idx"][:4])
+        L = owq.OwqLinear(d, device=dev, layout=owq.OWQ_LAYOUT_TC)
+        rows = sorted(set([0, 127, 128, M - 1] + list(np.random.default_rng(i).choice(M, 60, replace=False))))
+        runs.append(dict(L=L, x=torch.from_numpy(x).to(dev), y=torch.empty((B, M), dtype=torch.float32, device=dev),
+                         rows=rows, ref=O.matvec_rows(rep_from_synth(d), x.astype(np.float64), rows)))
+    torch.cuda.synchronize()
+    for it in range(20):
+        for sd, r in zip(streams, runs):
+            with torch.cuda.stream(sd):
+                r["L"](r["x"], y=r["y"], y_f32=True)
+    torch.cuda.synchronize()
+    for r in runs:
+        e, _ = rel_err(r["y"].cpu().numpy().astype(np.float64)[:, r["rows"]], r["ref"])
+        assert e <= TOL
+
+
 def test_workspace_sync_words_left_zero(dev):
     """One workspace shared by calls of different shapes, batches and grids --
     co-resident (zero-word slot protocol) and larger than the SM count (counter
